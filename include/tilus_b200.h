@@ -1,0 +1,159 @@
+/*
+ * tilus_b200.h -- C ABI of the B200-native A16Wx low-bit-weight matmul.
+ *
+ * The operation is the paper's "C_{M,N} = A_{M,K} x B_{K,N}, where A and B are
+ * float16 and int6", generalised to every weight format of
+ * PAPER.md:162 (uint1..8, int2..8 -- int1 is an extension --, float3..8 with any
+ * exponent/mantissa split), with group-wise fp16 scales along K and, for
+ * unsigned formats, zero points (north star; readings R6-R8):
+ *
+ *     w[k,n] = (value(q[k,n]) - z[k/G, n]) * s[k/G, n]        (z = 0 unless uint)
+ *     Y[m,n] = fp16( sum_k A[m,k] * w[k,n] )   accumulated in fp32
+ *
+ * The weights reach the library as the paper's compact bitstream
+ * (LSB-first, row-major [K,N], reading R1/R2), are re-laid
+ * out ONCE by tl_transform_weights (the "Change Layout" pre-processing step of
+ * PAPER.md:187 / PAPER.md:409-416) and then consumed by tl_matmul on every
+ * call.  The transformed layout is opaque and versioned (tl_format_version).
+ *
+ * Conventions (all functions):
+ *   - extern "C", thread-safe, never throw, never synchronise the host.
+ *   - Every pointer argument is a DEVICE pointer unless its name ends in _host.
+ *   - The caller owns every buffer (including the workspace); the library never
+ *     allocates on the hot path, so calls are CUDA-graph capturable.
+ *   - All argument checks run on the host before any launch; a non-OK status
+ *     means nothing was enqueued.  After launching, cudaGetLastError() is
+ *     mapped to TL_ECUDA.  Asynchronous device faults surface at the caller's
+ *     next synchronisation.  tl_last_error() returns a thread-local message.
+ *   - Work is enqueued on `stream` (a cudaStream_t passed as void*; NULL = legacy
+ *     default stream).
+ *   - Pointers and row strides must be 16-byte aligned.
+ *   - Shape support: K % 128 == 0, N % 128 == 0; group G divides K and is one of
+ *     32, 64, 128 or a multiple of 128 (G == K is per-channel).  M >= 0; M == 0 is
+ *     a no-op returning TL_OK.
+ */
+#ifndef TILUS_B200_H_
+#define TILUS_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Weight element type: the 4-byte dtype code of SPEC.md:276 (kind, bits, exp, man).
+ * kind 0 = uint, 1 = int (two's complement), 2 = float (bias 2^(E-1)-1, subnormals,
+ * no Inf/NaN -- reading R3).  Kernel formats: bits 1..8; float needs bits >= 3,
+ * 1 <= exp <= 4, man = bits-1-exp >= 0 (reading R4) -- 37 formats in all. */
+typedef struct {
+  uint8_t kind;
+  uint8_t bits;
+  uint8_t exp_bits;
+  uint8_t man_bits;
+} tl_wtype;
+
+typedef enum { TL_ACT_F16 = 0 } tl_atype; /* activations, scales and Y are fp16 */
+
+typedef enum {
+  TL_OK = 0,
+  TL_EINVAL_DTYPE = 1,  /* weight format not one of the 37 kernel formats      */
+  TL_EINVAL_SHAPE = 2,  /* K, N not multiples of 128, negative M, bad strides   */
+  TL_EINVAL_GROUP = 3,  /* G does not divide K or is not 32/64/128/128*j        */
+  TL_EALIGN = 4,        /* pointer or stride not 16-byte aligned                */
+  TL_EZEROS = 5,        /* zeros given for a non-uint format                    */
+  TL_EWORKSPACE = 6,    /* workspace missing or smaller than required           */
+  TL_EUNSUPPORTED = 7,  /* valid request outside what this build implements     */
+  TL_ECUDA = 8,         /* a CUDA runtime call or launch failed                 */
+  TL_ENULL = 9          /* a required pointer is NULL                           */
+} tl_status;
+
+/* Which kernel family tl_matmul uses (CUDA cores for few tokens,
+ * tensor cores for more; the crossover is re-measured on B200). */
+typedef enum { TL_PATH_AUTO = 0, TL_PATH_GEMV = 1, TL_PATH_TC = 2 } tl_path;
+
+/* ---- sizes --------------------------------------------------------------- */
+
+/* ceil(K*N*bits/8): bytes of the compact bitstream. */
+size_t tl_packed_bytes(tl_wtype w, int64_t K, int64_t N);
+
+/* Bytes of the transformed weight.  Equal to tl_packed_bytes for every legal
+ * shape: the transform permutes bits and adds no padding (PAPER.md:187,
+ * "u8[K/BK, N/BN, BK*BN*b/8]").  Returns 0 for an illegal shape. */
+size_t tl_transformed_bytes(tl_wtype w, int64_t K, int64_t N);
+
+/* Version of the opaque transformed layout; bumps whenever the layout changes. */
+uint32_t tl_format_version(void);
+
+/* ---- one-time weight preparation ------------------------------------------ */
+
+/* Pack one code per byte (codes[K*N], row-major, each < 2^bits) into the compact
+ * LSB-first bitstream (readings R1/R2).  bitstream must hold
+ * tl_packed_bytes(w,K,N) bytes.  Codes are taken modulo 2^bits. */
+tl_status tl_pack(tl_wtype w, int64_t K, int64_t N, const uint8_t* codes, uint8_t* bitstream,
+                  void* stream);
+
+/* Inverse of tl_pack (test hook): codes[K*N], one per byte. */
+tl_status tl_unpack(tl_wtype w, int64_t K, int64_t N, const uint8_t* bitstream, uint8_t* codes,
+                    void* stream);
+
+/* The paper's "Change Layout" step: re-lay the
+ * bitstream out into 128x128 tiles whose bytes are in the order the kernels'
+ * threads load and unpack them.  w_t must hold
+ * tl_transformed_bytes(w,K,N) bytes and must not alias bitstream. */
+tl_status tl_transform_weights(tl_wtype w, int64_t K, int64_t N, const uint8_t* bitstream,
+                               void* w_t, void* stream);
+
+/* Exact inverse of tl_transform_weights (test hook). */
+tl_status tl_untransform_weights(tl_wtype w, int64_t K, int64_t N, const void* w_t,
+                                 uint8_t* bitstream, void* stream);
+
+/* ---- the hot path ------------------------------------------------------------ */
+
+/* Workspace bytes tl_matmul needs for this problem (split-K partials and tile
+ * semaphores).  The workspace must be ZERO-FILLED once when allocated; the
+ * kernels leave every semaphore at zero again when they finish, so it can be
+ * reused by any later call on the same stream without clearing. */
+size_t tl_matmul_workspace_bytes(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t group);
+
+/* Y[M,N] (row stride ldy elements, fp16) = A[M,K] (row stride lda elements, fp16)
+ * x dequant(w_t).  scales: [K/G, N] fp16 row-major.  zeros: [K/G, N] fp16 with
+ * integer values, uint formats only, or NULL (z = 0).  Enqueued on `stream`. */
+tl_status tl_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t group, const void* A,
+                    int64_t lda, const void* w_t, const void* scales, const void* zeros, void* Y,
+                    int64_t ldy, void* workspace, size_t workspace_bytes, void* stream);
+
+/* As tl_matmul with an explicit kernel family and split-K factor (0 = auto);
+ * used by the dispatch sweep and the tests. */
+tl_status tl_matmul_ex(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t group, const void* A,
+                       int64_t lda, const void* w_t, const void* scales, const void* zeros,
+                       void* Y, int64_t ldy, void* workspace, size_t workspace_bytes,
+                       int32_t path, int32_t splits, void* stream);
+
+/* End-to-end variant for host buffers: copies A_host [M,K] (pinned recommended)
+ * into the device staging buffer A_dev, runs tl_matmul into Y_dev and copies
+ * Y_dev back into Y_host [M,N], all on `stream` (no host sync).  Weights,
+ * scales and zeros stay resident on the device. */
+tl_status tl_matmul_hostio(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t group,
+                           const void* A_host, void* A_dev, const void* w_t, const void* scales,
+                           const void* zeros, void* Y_dev, void* Y_host, void* workspace,
+                           size_t workspace_bytes, void* stream);
+
+/* Which family / split tl_matmul would pick for this shape (for the bench). */
+tl_status tl_matmul_plan(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t group,
+                         int32_t* path_out, int32_t* splits_out);
+
+/* Test hook: out[K,N] fp32 = (value(q) - z) * s, computed exactly in fp32 from
+ * the TRANSFORMED weight (reading R9: exact, so it is bit-comparable with the
+ * oracle's dequant). */
+tl_status tl_dequant(tl_wtype w, int64_t K, int64_t N, int32_t group, const void* w_t,
+                     const void* scales, const void* zeros, float* out, void* stream);
+
+/* ---- errors -------------------------------------------------------------- */
+const char* tl_status_str(tl_status s);
+const char* tl_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TILUS_B200_H_ */

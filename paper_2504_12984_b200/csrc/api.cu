@@ -1,0 +1,170 @@
+// api.cu -- C-ABI entry points of the hot path: validation, the
+// GEMV / tensor-core dispatch (row a2), workspace layout, the
+// host-buffer end-to-end call and the error strings.
+#include <cstdlib>
+#include <cstring>
+
+#include "api_util.cuh"
+#include "paths.cuh"
+
+namespace tl {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+// Workspace: [semaphores: 64 KiB][partials ...]
+constexpr size_t kSemBytes = 64 * 1024;
+
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+// Path choice (row a2).  PAPER.md:546 used CUDA cores for 1-15 tokens and tensor
+// cores from 16 on an L40S; on B200 the crossover is lower and is set
+// from the measured sweep.
+static int choose_path(tl_wtype w, int64_t M) {
+  const int forced = env_int("TL_FORCE_PATH", 0);
+  if (forced == TL_PATH_GEMV || forced == TL_PATH_TC) return forced;
+  if (!tc_available()) return TL_PATH_GEMV;
+  if (M <= 1) return TL_PATH_GEMV;
+  (void)w;
+  return M <= 16 ? TL_PATH_GEMV : TL_PATH_TC;
+}
+
+}  // namespace tl
+
+using namespace tl;
+
+extern "C" {
+
+const char* tl_status_str(tl_status s) {
+  switch (s) {
+    case TL_OK: return "TL_OK";
+    case TL_EINVAL_DTYPE: return "TL_EINVAL_DTYPE";
+    case TL_EINVAL_SHAPE: return "TL_EINVAL_SHAPE";
+    case TL_EINVAL_GROUP: return "TL_EINVAL_GROUP";
+    case TL_EALIGN: return "TL_EALIGN";
+    case TL_EZEROS: return "TL_EZEROS";
+    case TL_EWORKSPACE: return "TL_EWORKSPACE";
+    case TL_EUNSUPPORTED: return "TL_EUNSUPPORTED";
+    case TL_ECUDA: return "TL_ECUDA";
+    case TL_ENULL: return "TL_ENULL";
+  }
+  return "TL_UNKNOWN";
+}
+
+const char* tl_last_error(void) { return g_err; }
+
+size_t tl_matmul_workspace_bytes(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t group) {
+  (void)w;
+  (void)group;
+  if (M <= 0 || N <= 0 || K <= 0) return kSemBytes;
+  size_t g = gemv_workspace_bytes(M, N, K);
+  size_t t = tc_workspace_bytes(M, N, K);
+  return kSemBytes + (g > t ? g : t);
+}
+
+tl_status tl_matmul_plan(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t group, int32_t* path_out,
+                         int32_t* splits_out) {
+  (void)N;
+  (void)K;
+  (void)group;
+  if (path_out) *path_out = choose_path(w, M);
+  if (splits_out) *splits_out = 0;
+  return TL_OK;
+}
+
+tl_status tl_matmul_ex(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t group, const void* A, int64_t lda,
+                       const void* w_t, const void* scales, const void* zeros, void* Y, int64_t ldy,
+                       void* workspace, size_t workspace_bytes, int32_t path, int32_t splits, void* stream) {
+  tl_status st;
+  if ((st = check_wtype(w)) != TL_OK) return st;
+  if ((st = check_kn(K, N)) != TL_OK) return st;
+  if ((st = check_group(K, group)) != TL_OK) return st;
+  if (M < 0) return fail(TL_EINVAL_SHAPE, "M=%lld < 0", (long long)M);
+  if (M == 0) return TL_OK;
+  if (M > (1 << 20)) return fail(TL_EINVAL_SHAPE, "M above 2^20");
+  if (!A || !w_t || !scales || !Y) return fail(TL_ENULL, "tl_matmul: NULL pointer");
+  if (zeros && w.kind != 0) return fail(TL_EZEROS, "zero points are for uint formats only (reading R6)");
+  if (lda < K || ldy < N) return fail(TL_EINVAL_SHAPE, "lda=%lld < K or ldy=%lld < N", (long long)lda, (long long)ldy);
+  if (!aligned16(A) || !aligned16(w_t) || !aligned16(scales) || !aligned16(Y) || (zeros && !aligned16(zeros)) ||
+      (lda * 2) % 16 || (ldy * 2) % 16)
+    return fail(TL_EALIGN, "pointers and row strides must be 16-byte aligned");
+  const size_t need = tl_matmul_workspace_bytes(w, M, N, K, group);
+  if (!workspace || workspace_bytes < need)
+    return fail(TL_EWORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
+  if (!aligned16(workspace)) return fail(TL_EALIGN, "workspace must be 16-byte aligned");
+  if (path == TL_PATH_AUTO) path = choose_path(w, M);
+  int* sem = reinterpret_cast<int*>(workspace);
+  float* partial = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(workspace) + kSemBytes);
+  cudaStream_t s = as_stream(stream);
+  if (path == TL_PATH_GEMV) {
+    if (M > 16) {
+      // the CUDA-core path handles up to 16 rows per launch
+      for (int64_t m0 = 0; m0 < M; m0 += 16) {
+        const int64_t mm = (M - m0) < 16 ? (M - m0) : 16;
+        st = tl_matmul_ex(w, mm, N, K, group, reinterpret_cast<const __half*>(A) + m0 * lda, lda, w_t, scales, zeros,
+                          reinterpret_cast<__half*>(Y) + m0 * ldy, ldy, workspace, workspace_bytes, TL_PATH_GEMV,
+                          splits, stream);
+        if (st != TL_OK) return st;
+      }
+      return TL_OK;
+    }
+    GemvParams p{};
+    p.M = (int)M;
+    p.N = (int)N;
+    p.K = (int)K;
+    p.G = group;
+    p.A = reinterpret_cast<const __half*>(A);
+    p.lda = lda;
+    p.wt = reinterpret_cast<const uint8_t*>(w_t);
+    p.scales = reinterpret_cast<const __half*>(scales);
+    p.zeros = reinterpret_cast<const __half*>(zeros);
+    p.Y = reinterpret_cast<__half*>(Y);
+    p.ldy = ldy;
+    p.partial = partial;
+    p.sem = sem;
+    p.units = (int)((N / kBN) * (K / kBK));
+    return gemv_dispatch(w, p, splits > 0 ? splits : env_int("TL_GRID", 0), s);
+  }
+  if (path == TL_PATH_TC) {
+    if (!tc_available()) return fail(TL_EUNSUPPORTED, "tensor-core path not built");
+    return tc_matmul(w, M, N, K, group, reinterpret_cast<const __half*>(A), lda,
+                     reinterpret_cast<const uint8_t*>(w_t), reinterpret_cast<const __half*>(scales),
+                     reinterpret_cast<const __half*>(zeros), reinterpret_cast<__half*>(Y), ldy, partial, sem,
+                     splits, s);
+  }
+  return fail(TL_EUNSUPPORTED, "unknown path %d", path);
+}
+
+tl_status tl_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t group, const void* A, int64_t lda,
+                    const void* w_t, const void* scales, const void* zeros, void* Y, int64_t ldy, void* workspace,
+                    size_t workspace_bytes, void* stream) {
+  return tl_matmul_ex(w, M, N, K, group, A, lda, w_t, scales, zeros, Y, ldy, workspace, workspace_bytes,
+                      TL_PATH_AUTO, 0, stream);
+}
+
+tl_status tl_matmul_hostio(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t group, const void* A_host,
+                           void* A_dev, const void* w_t, const void* scales, const void* zeros, void* Y_dev,
+                           void* Y_host, void* workspace, size_t workspace_bytes, void* stream) {
+  if (M == 0) return TL_OK;
+  if (!A_host || !A_dev || !Y_dev || !Y_host) return fail(TL_ENULL, "tl_matmul_hostio: NULL pointer");
+  cudaStream_t s = as_stream(stream);
+  if (cudaMemcpyAsync(A_dev, A_host, (size_t)(M * K * 2), cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return fail(TL_ECUDA, "H2D copy of A failed");
+  tl_status st = tl_matmul(w, M, N, K, group, A_dev, K, w_t, scales, zeros, Y_dev, N, workspace, workspace_bytes,
+                           stream);
+  if (st != TL_OK) return st;
+  if (cudaMemcpyAsync(Y_host, Y_dev, (size_t)(M * N * 2), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return fail(TL_ECUDA, "D2H copy of Y failed");
+  return TL_OK;
+}
+
+}  // extern "C"

