@@ -1,0 +1,397 @@
+"""bench.py -- A16Wx low-bit-weight matmul on B200 (the hot path of Tilus, arXiv 2504.12984).
+
+Metric (BASELINE.json): "A16Wx matmul HBM GB/s & TFLOP/s vs bit width, batch 1/16/128,
+Llama-70B layers".  Workload (BASELINE.json configs[2]): the four Llama-3.3-70B linear
+layers (qkv 8192->10240, o 8192->8192, gate_up 8192->57344, down 28672->8192) in the
+four formats u3, i5, f6e3m2, u8, group 128, uint formats with zero points.
+
+A STEP is one pass of the whole hot path over one batch: 16 tl_matmul calls (4 layers x
+4 formats) at batch M (default 1 = decode).  `value` = algorithmic bytes of the step
+(packed weights + scales/zeros + A + Y) / device time, in GB/s.  Each step
+streams ~2.5 GB of weights, far more than the 126 MB L2, so no flush is needed between
+steps (inputs larger than L2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--M 1] [--impl ours|reference]
+
+Multi-GPU (torchrun, one process per GPU): weak scaling -- rank r owns its own
+column shard (the full layer width of the single-GPU problem) of a P-times wider
+layer, computes it with no communication, and (only with --gather) all-gathers Y over
+NCCL.  Time is the max over ranks of the device time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workloads as wl  # noqa: E402
+
+METRIC = "A16Wx matmul HBM GB/s & TFLOP/s vs bit width, batch 1/16/128, Llama-70B layers"
+WORKLOAD = "llama-3.3-70b linear layers (qkv,o,gate_up,down) x {u3,i5,f6e3m2,u8}, group 128 (BASELINE configs[2])"
+
+
+def alg_bytes(fmt: str, M: int, K: int, N: int, G: int) -> int:
+    """Algorithmic bytes of one matmul: packed codes + scales (+zeros) + A + Y."""
+    b = int(fmt[1])
+    zp = 1 if fmt[0] == "u" else 0
+    return K * N * b // 8 + (K // G) * N * 2 * (1 + zp) + 2 * M * K + 2 * M * N
+
+
+def load_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"], "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """NVML sampler of SM clock + throttle reasons, run DURING the timed region."""
+
+    REASONS = {
+        0x0000000000000001: "gpu_idle", 0x0000000000000002: "applications_clocks_setting",
+        0x0000000000000004: "sw_power_cap", 0x0000000000000008: "hw_slowdown", 0x0000000000000010: "sync_boost",
+        0x0000000000000020: "sw_thermal_slowdown", 0x0000000000000040: "hw_thermal_slowdown",
+        0x0000000000000080: "hw_power_brake_slowdown", 0x0000000000000100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int, period_s: float = 0.002):
+        self.index, self.period = index, period_s
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # pragma: no cover - no NVML
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            self._sample()
+            time.sleep(self.period)
+
+    def _sample(self):
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for bit, name in self.REASONS.items():
+                if r & bit and name != "gpu_idle":
+                    self.reasons.add(name)
+        except Exception:
+            pass
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self._stop.set()
+            self._t.join()
+            self._sample()
+
+    def summary(self) -> dict:
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------------------
+def cpu_baseline(formats, layers, G, M, budget_s=12.0, impl_line=False):
+    """The oracle as it stands, on the host cores, over a bounded column sample of the workload."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import dequant, matmul_fp64, parse_wtype
+    rng = np.random.default_rng(0)
+    tot_bytes, tot_t = 0, 0.0
+    cols = 64
+    with threadpool_limits(limits=1):
+        t_start = time.perf_counter()
+        passes = 0
+        while True:
+            for fmt in formats:
+                for lname, (K, N) in layers.items():
+                    seed = wl.stable_seed("cpu", fmt, lname)
+                    codes = wl.gen_codes(fmt, K, cols, seed)
+                    s = wl.gen_scales(fmt, K, cols, G, seed)
+                    z = wl.gen_zeros(fmt, K, cols, G, seed)
+                    A = wl.gen_activations(M, K, seed)
+                    t0 = time.perf_counter()
+                    matmul_fp64(A, dequant(parse_wtype(fmt), codes, s, z, G))
+                    tot_t += time.perf_counter() - t0
+                    tot_bytes += alg_bytes(fmt, M, K, cols, G)
+            passes += 1
+            if time.perf_counter() - t_start > budget_s or passes >= 50:
+                break
+    del rng
+    return {"value": tot_bytes / tot_t / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"{passes} pass(es) over {len(formats)}x{len(layers)} (format, layer) pairs, "
+                      f"{cols} columns each, M={M}, numpy fp64, 1 thread; {tot_t:.1f} s of oracle time"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle timed as it stands on the host cores, same metric/config."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    formats, layers = args.formats, {k: wl.LLAMA33_70B[k] for k in args.layers}
+    for _ in range(args.warmup):
+        cpu_baseline(formats, layers, 128, args.M, budget_s=0.0)
+    t0 = time.perf_counter()
+    vals = []
+    for _ in range(args.steps):
+        vals.append(cpu_baseline(formats, layers, 128, args.M, budget_s=0.0))
+    dt = time.perf_counter() - t0
+    v = statistics.median([x["value"] for x in vals])
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "M": args.M, "formats": formats, "layers": list(layers),
+                       "group": 128, "sample": "64 columns per (format, layer)"},
+            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                             "sample": vals[0]["sample"]},
+            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_12984_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    G = 128
+    M = args.M
+    layers = {k: wl.LLAMA33_70B[k] for k in args.layers}
+
+    # ---- one-time weight preparation (untimed) ----
+    probs = []
+    for fmt in args.formats:
+        w = P.wtype(fmt)
+        for lname, (K, N) in layers.items():
+            seed = wl.stable_seed("bench", fmt, lname, rank)
+            codes = wl.gen_codes_torch(fmt, K, N, seed, dev)
+            bs = P.tl_pack(w, K, N, codes)
+            del codes
+            wt = P.tl_transform_weights(w, K, N, bs)
+            del bs
+            s = wl.gen_scales_torch(fmt, K, N, G, seed, dev)
+            z = wl.gen_zeros_torch(fmt, K, N, G, seed, dev)
+            probs.append({"fmt": fmt, "layer": lname, "K": K, "N": N, "w": w, "wt": wt, "s": s, "z": z})
+    torch.cuda.synchronize()
+    ws_bytes = max(P.tl_matmul_workspace_bytes(p["w"], max(M, 128), p["N"], p["K"], G) for p in probs)
+    ws = torch.zeros(ws_bytes, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def make_io(m):
+        for p in probs:
+            p["A"] = wl.gen_activations_torch(m, p["K"], wl.stable_seed("A", p["layer"], m, rank), dev)
+            p["Y"] = torch.empty((m, p["N"]), dtype=torch.float16, device=dev)
+            p["Yg"] = torch.empty((world, m, p["N"]), dtype=torch.float16, device=dev) if args.gather else None
+
+    def step(m, events=None):
+        for i, p in enumerate(probs):
+            if events is not None:
+                events[i][0].record(stream)
+            P.tl_matmul(p["w"], m, p["N"], p["K"], G, p["A"], p["wt"], p["s"], p["z"], p["Y"], ws)
+            if events is not None:
+                events[i][1].record(stream)
+            if args.gather:
+                dist.all_gather_into_tensor(p["Yg"], p["Y"])
+
+    def timed(m, steps, warmup, per_launch=True, sampler=None):
+        make_io(m)
+        for _ in range(warmup):
+            step(m)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in probs]
+               for _ in range(steps)] if per_launch else None
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ctx = sampler if sampler is not None else _Null()
+        with ctx:
+            t0.record(stream)
+            for k in range(steps):
+                step(m, evs[k] if per_launch else None)
+            t1.record(stream)
+            torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = t0.elapsed_time(t1)
+        launch_ms = None
+        if per_launch:
+            launch_ms = [[e[0].elapsed_time(e[1]) for e in row] for row in evs]
+        ms_max = ms
+        if world > 1:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_max = float(t.item())
+        return ms_max, launch_ms
+
+    peaks = load_peaks()
+    sampler = ClockSampler(local)
+    ms, launch_ms = timed(M, args.steps, args.warmup, per_launch=True, sampler=sampler)
+    step_bytes = sum(alg_bytes(p["fmt"], M, p["K"], p["N"], G) for p in probs)
+    step_flops = sum(2 * M * p["K"] * p["N"] for p in probs)
+    ms_per_step = ms / args.steps
+    value = world * step_bytes / (ms_per_step * 1e-3) / 1e9
+
+    # per-(format, layer) detail and the dominant kernel's roofline
+    path_names = {1: "gemv", 2: "tc"}
+    details = []
+    fam_bytes, fam_ms = {}, {}
+    for i, p in enumerate(probs):
+        lm = statistics.mean(row[i] for row in launch_ms)
+        b = alg_bytes(p["fmt"], M, p["K"], p["N"], G)
+        path, _ = P.tl_matmul_plan(p["w"], M, p["N"], p["K"], G)
+        fam = path_names.get(path, str(path))
+        fam_bytes[fam] = fam_bytes.get(fam, 0) + b
+        fam_ms[fam] = fam_ms.get(fam, 0.0) + lm
+        details.append({"fmt": p["fmt"], "layer": p["layer"], "M": M, "us": round(lm * 1e3, 2),
+                        "GBps": round(b / (lm * 1e-3) / 1e9, 1),
+                        "hbm_frac": round(b / (lm * 1e-3) / 1e9 / peaks["hbm_gbs"], 3), "path": fam})
+    dom = max(fam_ms, key=fam_ms.get)
+    achieved = fam_bytes[dom] / (fam_ms[dom] * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(f"{dom}_M{M}")
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic, "kernel": dom,
+                "peak_source": peaks["source"], "share_of_step": round(fam_ms[dom] / (ms_per_step), 3)}
+
+    # ---- extra batch sizes (reported, not part of `value`) ----
+    extra = []
+    if not args.no_extra:
+        for m2 in [x for x in (16, 64, 128) if x != M]:
+            ms2, lms2 = timed(m2, max(3, min(args.steps, 10)), 2, per_launch=True)
+            for i, p in enumerate(probs):
+                lm = statistics.mean(row[i] for row in lms2)
+                b = alg_bytes(p["fmt"], m2, p["K"], p["N"], G)
+                fl = 2 * m2 * p["K"] * p["N"]
+                extra.append({"fmt": p["fmt"], "layer": p["layer"], "M": m2, "us": round(lm * 1e3, 2),
+                              "GBps": round(b / (lm * 1e-3) / 1e9, 1),
+                              "TFLOPs": round(fl / (lm * 1e-3) / 1e12, 2),
+                              "tensor_frac_fp16": round(fl / (lm * 1e-3) / 1e12 / peaks["bf16_tflops"], 3)})
+        make_io(M)
+
+    # ---- end to end through the public C-ABI with host buffers (A in, Y out every call) ----
+    e2e = None
+    if not args.no_e2e:
+        make_io(M)
+        host = []
+        for p in probs:
+            Ah = torch.empty((M, p["K"]), dtype=torch.float16, pin_memory=True)
+            Ah.copy_(p["A"].cpu())
+            Yh = torch.empty((M, p["N"]), dtype=torch.float16, pin_memory=True)
+            host.append((Ah, Yh))
+
+        def step_e2e():
+            for p, (Ah, Yh) in zip(probs, host):
+                P.tl_matmul_hostio(p["w"], M, p["N"], p["K"], G, Ah, p["A"], p["wt"], p["s"], p["z"], p["Y"], Yh, ws)
+
+        for _ in range(args.warmup):
+            step_e2e()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            step_e2e()
+        t1.record(stream)
+        torch.cuda.synchronize()
+        ems = t0.elapsed_time(t1)
+        if world > 1:
+            t = torch.tensor([ems], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": round(world * step_bytes / (ems / args.steps * 1e-3) / 1e9, 1), "unit": "GB/s",
+               "h2d_bytes_per_step": sum(2 * M * p["K"] for p in probs),
+               "d2h_bytes_per_step": sum(2 * M * p["N"] for p in probs),
+               "ms_per_step": round(ems / args.steps, 4)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f16", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "M": M, "formats": args.formats, "layers": list(layers), "group": 128,
+                       "weights": "uint formats with fp16 zero points; int/float symmetric",
+                       "l2": "inputs larger than L2: each step streams %.2f GB of weights (L2 126 MB)" %
+                             (step_bytes / 1e9),
+                       "parallelism": f"column shards, {world} rank(s), no data-path collective" +
+                                      (" + NCCL all-gather of Y" if args.gather else ""),
+                       "tflops_at_M": round(step_flops / (ms_per_step * 1e-3) / 1e12, 3)},
+            "roofline": roofline,
+            "e2e": e2e,
+            "gpu_launches": args.steps * len(probs),
+            "clocks": sampler.summary(),
+            "details": details,
+            "details_extra_M": extra,
+        }
+        if world == 1 and not args.no_cpu:
+            line["cpu_baseline"] = cpu_baseline(args.formats, layers, G, M)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--M", type=int, default=1)
+    ap.add_argument("--formats", nargs="+", default=wl.CONFIG2["formats"])
+    ap.add_argument("--layers", nargs="+", default=list(wl.LLAMA33_70B))
+    ap.add_argument("--gather", action="store_true")
+    ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -132,6 +132,7 @@ tl_status tl_matmul_ex(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t grou
     p.partial = partial;
     p.sem = sem;
     p.units = (int)((N / kBN) * (K / kBK));
+    p.magic = 0x64006400u;
     return gemv_dispatch(w, p, splits > 0 ? splits : env_int("TL_GRID", 0), s);
   }
   if (path == TL_PATH_TC) {

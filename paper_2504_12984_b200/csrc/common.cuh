@@ -156,15 +156,32 @@ struct PairConsts {
   // uint/int: hz[P] = -(2^(10-P) + z) as fp16x2 for every P in [0, 10]
   // float   : unused
   __half2 neg_off[11];
+  // 0x64006400 (fp16 1024.0 in both halves), passed in from a kernel argument so the
+  // compiler keeps it in a register and fuses AND-mask + OR-magic into ONE LOP3
+  uint32_t magic;
 };
+
+// Is P used by any pair of a b-bit column run?  (Only those constants are built.)
+template <int B>
+__host__ __device__ constexpr bool pair_p_used(int P) {
+  for (int i = 0; i < 64; ++i) {
+    const int w = seg_width(B, 0), per_word = 32 / w;
+    const int o0 = (((2 * i) % per_word) >> 1) * w;
+    const int v = (o0 + B <= 10) ? o0 : ((o0 >= 8 && o0 - 8 + B <= 10) ? o0 - 8 : 0);
+    if (v == P) return true;
+  }
+  return false;
+}
 
 template <class F>
 __device__ __forceinline__ void make_pair_consts(PairConsts& c, float z) {
   if constexpr (F::kind != kFloat) {
 #pragma unroll
     for (int P = 0; P <= 10; ++P) {
-      const __half h = __float2half_rn(-(float)(1 << (10 - P)) - z);
-      c.neg_off[P] = __halves2half2(h, h);
+      if (pair_p_used<F::bits>(P)) {
+        const __half h = __float2half_rn(-(float)(1 << (10 - P)) - z);
+        c.neg_off[P] = __halves2half2(h, h);
+      }
     }
   }
 }
@@ -173,7 +190,7 @@ template <class F, int I>
 __device__ __forceinline__ __half2 pair_value(const uint32_t* words, const PairConsts& c) {
   if constexpr (F::kind != kFloat) {
     constexpr int P = PairP<F::bits, I>::value;
-    const uint32_t x = assemble_pair<F::bits, I, P>(words) | 0x64006400u;  // 1024 + 2^P u
+    const uint32_t x = assemble_pair<F::bits, I, P>(words) | c.magic;  // 1024 + 2^P u
     constexpr uint32_t sc = (uint32_t)(15 - P) << 10;                   // fp16 bits of 2^-P
     return __hfma2(u32_as_h2(x), u32_as_h2(sc | (sc << 16)), c.neg_off[P]);  // u - z, exact
   } else {

@@ -11,7 +11,7 @@ namespace tl {
 template <class F>
 __global__ void dequant_kernel(const uint8_t* __restrict__ wt, const __half* __restrict__ scales,
                                const __half* __restrict__ zeros, float* __restrict__ out, int64_t K, int64_t N,
-                               int G) {
+                               int G, uint32_t magic) {
   const int64_t KT = K / kBK;
   const int64_t tile = blockIdx.x;
   const int nl = threadIdx.x;
@@ -32,6 +32,7 @@ __global__ void dequant_kernel(const uint8_t* __restrict__ wt, const __half* __r
     }
   }
   PairConsts pc;
+  pc.magic = magic;
   int gcur = -1;
   float s = 0.f;
   static_for<0, 64>([&](auto I) {
@@ -55,7 +56,7 @@ __global__ void dequant_kernel(const uint8_t* __restrict__ wt, const __half* __r
 template <class F>
 void launch_dequant(const uint8_t* wt, const __half* scales, const __half* zeros, float* out, int64_t K, int64_t N,
                     int G, unsigned tiles, cudaStream_t st) {
-  dequant_kernel<F><<<tiles, kBN, 0, st>>>(wt, scales, zeros, out, K, N, G);
+  dequant_kernel<F><<<tiles, kBN, 0, st>>>(wt, scales, zeros, out, K, N, G, 0x64006400u);
 }
 
 }  // namespace tl

@@ -45,7 +45,7 @@ __device__ __forceinline__ float fhfma(uint16_t a, uint16_t b, float c) {
 }
 
 template <class F, int MT, int KH>
-__device__ __forceinline__ void gemv_tile_half(const uint8_t* stage, int c, int kt, int G, bool has_zeros,
+__device__ __forceinline__ void gemv_tile_half(const uint8_t* stage, int c, uint32_t magic, int G, bool has_zeros,
                                                float (&tot)[MT]) {
   using L = GemvLayout<F, MT>;
   constexpr int B = F::bits;
@@ -76,19 +76,18 @@ __device__ __forceinline__ void gemv_tile_half(const uint8_t* stage, int c, int 
   const __half* As = reinterpret_cast<const __half*>(stage + L::w_bytes);
   const __half* Ss = reinterpret_cast<const __half*>(stage + L::w_bytes + L::a_bytes);
   const __half* Zs = reinterpret_cast<const __half*>(stage + L::w_bytes + L::a_bytes + L::sz_bytes);
-  const int spl = G < 64 ? G : 64;         // sub-piece length (k) inside this half
-  const int row0 = (G >= kBK) ? 0 : 0;     // group row of the tile's first k in the stage
-  (void)row0;
+  // sub-pieces of 32 k (16 pairs): every group boundary (G = 32, 64, 128*j) is one
+  const int lg = G == 32 ? 5 : 6;          // log2 G for G < 128
   float acc[MT];
 #pragma unroll
   for (int m = 0; m < MT; ++m) acc[m] = 0.f;
   PairConsts pc;
+  pc.magic = magic;
   float s = 0.f;
   static_for<0, 32>([&](auto II) {
     constexpr int i = KH * 32 + decltype(II)::value;
-    if ((2 * i) % spl == 0) {
-      // new sub-piece: its group row within the stage's scale slice
-      const int r = (G >= kBK) ? 0 : (2 * i) / G;
+    if constexpr (i % 16 == 0) {
+      const int r = (G >= kBK) ? 0 : ((2 * i) >> lg);  // group row of this sub-piece in the stage slice
       s = __half2float(Ss[r * kBN + c]);
       float z = 0.f;
       if constexpr (F::kind == kUint) z = has_zeros ? __half2float(Zs[r * kBN + c]) : 0.f;
@@ -103,7 +102,7 @@ __device__ __forceinline__ void gemv_tile_half(const uint8_t* stage, int c, int 
       acc[m] = fhfma(wlo, (uint16_t)(a2 & 0xFFFF), acc[m]);
       acc[m] = fhfma(whi, (uint16_t)(a2 >> 16), acc[m]);
     }
-    if ((2 * i + 2) % spl == 0) {
+    if constexpr (i % 16 == 15) {
 #pragma unroll
       for (int m = 0; m < MT; ++m) {
         tot[m] = fmaf(s, acc[m], tot[m]);
@@ -111,7 +110,6 @@ __device__ __forceinline__ void gemv_tile_half(const uint8_t* stage, int c, int 
       }
     }
   });
-  (void)kt;
 }
 
 template <class F, int MT>
@@ -157,12 +155,10 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvParams p) {
       const uint64_t pol_w = policy_evict_first();
       const uint64_t pol_a = policy_evict_last();
       const uint32_t bytes = L::w_bytes + p.M * kBK * 2 + spt * kBN * 2 * (has_zeros ? 2 : 1);
+      int s = 0, ph = 0, nt = u0 / KT, kt = u0 % KT;
       for (int u = u0; u < u1; ++u) {
-        const int t = u - u0;
-        const int s = t % NS;
-        if (t >= NS) mbar_wait(&empty[s], ((t / NS) - 1) & 1);
+        if (u - u0 >= NS) mbar_wait(&empty[s], ph ^ 1);
         uint8_t* st = stages + s * L::stage_bytes;
-        const int nt = u / KT, kt = u % KT;
         mbar_arrive_expect_tx(&full[s], bytes);
         tma_bulk_g2s(st, p.wt + (int64_t)u * L::w_bytes, L::w_bytes, &full[s], pol_w);
         for (int m = 0; m < p.M; ++m)
@@ -175,6 +171,8 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvParams p) {
             tma_bulk_g2s(st + L::w_bytes + L::a_bytes + L::sz_bytes + r * kBN * 2,
                          p.zeros + (int64_t)(g0 + r) * p.N + nt * kBN, kBN * 2, &full[s], pol_w);
         }
+        if (++kt == KT) { kt = 0; ++nt; }
+        if (++s == NS) { s = 0; ph ^= 1; }
       }
     }
     return;
@@ -187,20 +185,21 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvParams p) {
 #pragma unroll
   for (int m = 0; m < MT; ++m) tot[m] = 0.f;
 
+  int s = 0, ph = 0, nt = u0 / KT, kt = u0 % KT;
   for (int u = u0; u < u1; ++u) {
-    const int t = u - u0;
-    const int s = t % NS;
-    const int nt = u / KT, kt = u % KT;
-    mbar_wait(&full[s], (t / NS) & 1);
+    mbar_wait(&full[s], ph);
     const uint8_t* st = stages + s * L::stage_bytes;
-    if (kh == 0) gemv_tile_half<F, MT, 0>(st, c, kt, p.G, has_zeros, tot);
-    else gemv_tile_half<F, MT, 1>(st, c, kt, p.G, has_zeros, tot);
+    if (kh == 0) gemv_tile_half<F, MT, 0>(st, c, p.magic, p.G, has_zeros, tot);
+    else gemv_tile_half<F, MT, 1>(st, c, p.magic, p.G, has_zeros, tot);
     __syncwarp();
     if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+    if (++s == NS) { s = 0; ph ^= 1; }
+    const int cur_nt = nt, cur_kt = kt;
+    if (++kt == KT) { kt = 0; ++nt; }
 
-    const bool last_of_tile = (kt == KT - 1) || (u == u1 - 1);
+    const bool last_of_tile = (cur_kt == KT - 1) || (u == u1 - 1);
     if (!last_of_tile) continue;
-    // ---- flush n-tile nt: reduce the two k-halves, then write Y or a partial ----
+    // ---- flush n-tile cur_nt: reduce the two k-halves, then write Y or a partial ----
     if (kh == 1) {
 #pragma unroll
       for (int m = 0; m < MT; ++m) red[m * kBN + c] = tot[m];
@@ -209,8 +208,8 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvParams p) {
     if (kh == 0) {
 #pragma unroll
       for (int m = 0; m < MT; ++m) tot[m] += red[m * kBN + c];
-      const int n = nt * kBN + c;
-      const int ua = nt * KT, ub = ua + KT;  // units of this n-tile
+      const int n = cur_nt * kBN + c;
+      const int ua = cur_nt * KT, ub = ua + KT;  // units of this n-tile
       const bool complete = (u0 <= ua) && (u1 >= ub);
       if (complete) {
 #pragma unroll
@@ -218,7 +217,7 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvParams p) {
           if (m < p.M) p.Y[(int64_t)m * p.ldy + n] = __float2half_rn(tot[m]);
       } else {
         const int nt_first = u0 / KT;
-        const int slot = (nt == nt_first) ? 0 : 1;
+        const int slot = (cur_nt == nt_first) ? 0 : 1;
         float* part = p.partial + ((int64_t)(cta * 2 + slot) * p.M) * kBN;
 #pragma unroll
         for (int m = 0; m < MT; ++m)
@@ -229,7 +228,7 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvParams p) {
           // the CTAs whose ranges intersect [ua, ub) are owner(ua) .. owner(ub - 1)
           const int lo = (int)((((int64_t)ua + 1) * grid - 1) / p.units);
           const int hi = (int)((((int64_t)ub) * grid - 1) / p.units);
-          const int prev = atomicAdd(&p.sem[nt], 1);
+          const int prev = atomicAdd(&p.sem[cur_nt], 1);
           flag[0] = (prev == hi - lo) ? 1 : 0;
           flag[1] = lo;
           flag[2] = hi;
@@ -242,12 +241,12 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvParams p) {
             float sum = 0.f;
             for (int q = lo; q <= hi; ++q) {
               const int q_first = (int)((int64_t)q * p.units / grid) / KT;
-              const int qslot = (nt == q_first) ? 0 : 1;
+              const int qslot = (cur_nt == q_first) ? 0 : 1;
               sum += __ldcg(p.partial + ((int64_t)(q * 2 + qslot) * p.M + m) * kBN + c);
             }
             p.Y[(int64_t)m * p.ldy + n] = __float2half_rn(sum);
           }
-          if (c == 0) p.sem[nt] = 0;  // leave the semaphore clean for the next call
+          if (c == 0) p.sem[cur_nt] = 0;  // leave the semaphore clean for the next call
         }
       }
     }

@@ -18,6 +18,7 @@ struct GemvParams {
   float* partial;  // [grid][2][M][128] fp32 stream-K partial tiles
   int* sem;        // [N/128] self-resetting tile semaphores
   int units;       // (N/128) * (K/128)
+  uint32_t magic;  // 0x64006400 (see PairConsts::magic)
 };
 
 tl_status gemv_dispatch(tl_wtype w, const GemvParams& p, int grid_req, cudaStream_t st);

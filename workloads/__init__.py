@@ -136,3 +136,42 @@ def sample_columns(N: int, n_tile: int = 128, shards: int = 8, extra: int = 64, 
     rng = np.random.Generator(np.random.PCG64(seed + 5))
     cols.update(rng.integers(0, N, size=extra).tolist())
     return np.array(sorted(cols), dtype=np.int64)
+
+
+# --------------------------------------------------------------------------
+# device-side generators (same recipe, torch's Philox RNG) for bench-size layers
+# --------------------------------------------------------------------------
+def torch_generator(seed: int, device="cuda"):
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed & ((1 << 63) - 1))
+    return g
+
+
+def gen_codes_torch(fmt: str, K: int, N: int, seed: int, device="cuda"):
+    import torch
+    b = _bits_of(fmt)
+    return torch.randint(0, 1 << b, (K, N), generator=torch_generator(seed, device), device=device, dtype=torch.uint8)
+
+
+def gen_scales_torch(fmt: str, K: int, N: int, group: int, seed: int, device="cuda"):
+    import torch
+    b = _bits_of(fmt)
+    u = torch.rand((K // group, N), generator=torch_generator(seed + 1, device), device=device) + 0.5
+    return (u * (0.02 / (1 << (b - 1)))).to(torch.float16)
+
+
+def gen_zeros_torch(fmt: str, K: int, N: int, group: int, seed: int, device="cuda"):
+    import torch
+    if _kind_of(fmt) != "u":
+        return None
+    b = _bits_of(fmt)
+    lo = max((1 << (b - 1)) - 1, 0)
+    z = torch.randint(lo, (1 << (b - 1)) + 1, (K // group, N), generator=torch_generator(seed + 2, device),
+                      device=device)
+    return z.to(torch.float16)
+
+
+def gen_activations_torch(M: int, K: int, seed: int, device="cuda"):
+    import torch
+    return torch.randn((M, K), generator=torch_generator(seed + 3, device), device=device).to(torch.float16)
