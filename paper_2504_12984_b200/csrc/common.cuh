@@ -204,4 +204,30 @@ __device__ __forceinline__ __half2 pair_value(const uint32_t* words, const PairC
   }
 }
 
+// Load the segment words of column c, k-half KH (pairs [32*KH, 32*KH+32)) of one transformed
+// tile held in shared memory, into words[] at the positions assemble_pair<> reads.
+template <int B, int KH>
+__device__ __forceinline__ void load_half_words(const uint8_t* tile, int c, uint32_t* words) {
+#pragma unroll
+  for (int s = 0; s < num_segs(B); ++s) {
+    const int w = seg_width(B, s), base = seg_base(B, s);
+    const uint8_t* sp = tile + 2048 * base;
+    if (w == 1) {
+      const uint2 x = *reinterpret_cast<const uint2*>(sp + c * 16 + KH * 8);
+      words[4 * base + 2 * KH + 0] = x.x;
+      words[4 * base + 2 * KH + 1] = x.y;
+    } else {
+#pragma unroll
+      for (int v = 0; v < w / 2; ++v) {
+        const int vv = KH * (w / 2) + v;
+        const uint4 x = *reinterpret_cast<const uint4*>(sp + (vv * 128 + c) * 16);
+        words[4 * base + 4 * vv + 0] = x.x;
+        words[4 * base + 4 * vv + 1] = x.y;
+        words[4 * base + 4 * vv + 2] = x.z;
+        words[4 * base + 4 * vv + 3] = x.w;
+      }
+    }
+  }
+}
+
 }  // namespace tl

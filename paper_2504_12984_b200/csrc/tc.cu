@@ -1,10 +1,113 @@
-// tc.cu -- placeholder until the tcgen05 path lands.
-#include "paths.cuh"
+// tc.cu -- host side of the tensor-core path: shared-memory carve-up, the TMA tensor map
+// of the activations, m-chunking (MMA N <= 256) and the per-format dispatch.  The kernel
+// (tc.cuh) is instantiated one format per translation unit (build/gen/tc_*.cu).
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "tc.cuh"
+
 namespace tl {
-bool tc_available() { return false; }
-size_t tc_workspace_bytes(int64_t, int64_t, int64_t) { return 0; }
-tl_status tc_matmul(tl_wtype, int64_t, int64_t, int64_t, int32_t, const __half*, int64_t, const uint8_t*,
-                    const __half*, const __half*, __half*, int64_t, float*, int*, int, cudaStream_t) {
-  return TL_EUNSUPPORTED;
+
+template <class F>
+tl_status launch_tc(const TcParams& p, const CUtensorMap* tmap, int grid, uint32_t smem_bytes, cudaStream_t st);
+
+bool tc_available() { return true; }
+
+constexpr int kTcMaxCtas = 160;
+
+static int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+size_t tc_workspace_bytes(int64_t M, int64_t N, int64_t K) {
+  (void)N;
+  (void)K;
+  const int nb = round_up((int)(M < 256 ? M : 256), 16);
+  return (size_t)kTcMaxCtas * 2 * nb * 128 * 4;
 }
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+// A [M, K] fp16 row-major (row stride lda elements): boxes of 64 k x NB rows, 128B swizzle,
+// rows >= M zero-filled by the TMA unit.
+static tl_status make_tmap_a(CUtensorMap* m, const __half* A, int64_t M, int64_t K, int64_t lda, int NB) {
+  auto enc = get_encode();
+  if (!enc) return fail(TL_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
+  cuuint64_t strides[1] = {(cuuint64_t)(lda * 2)};
+  cuuint32_t box[2] = {64, (cuuint32_t)NB};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(A), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TL_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return TL_OK;
+}
+
+tl_status tc_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, const __half* A, int64_t lda,
+                    const uint8_t* wt, const __half* scales, const __half* zeros, __half* Y, int64_t ldy,
+                    float* partial, int* sem, int grid_req, cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (sms > kTcMaxCtas) sms = kTcMaxCtas;
+  for (int64_t m0 = 0; m0 < M; m0 += 256) {
+    const int mc = (int)((M - m0) < 256 ? (M - m0) : 256);
+    TcParams p{};
+    p.M = mc;
+    p.N = (int)N;
+    p.K = (int)K;
+    p.G = G;
+    p.NB = round_up(mc, 16);
+    p.units = (int)((N / kBN) * (K / kBK));
+    p.wt = wt;
+    p.scales = scales;
+    p.zeros = zeros;
+    p.Y = Y + m0 * ldy;
+    p.ldy = ldy;
+    p.partial = partial;
+    p.sem = sem;
+    p.magic = 0x64006400u;
+    int cols = 32;
+    while (cols < 2 * p.NB) cols <<= 1;
+    p.tmem_cols = (uint32_t)cols;
+    // shared memory: 2 x 32 KB dequant tiles, then NS x (activation boxes, packed tile, scale/zero slice)
+    const uint32_t wb = (uint32_t)tile_bytes(w.bits);
+    const uint32_t astage = (uint32_t)p.NB * 256;
+    const uint32_t budget = 227 * 1024 - 1024 - 256;
+    int ns = 8;
+    while (ns > 2 && 2 * kDeqBytes + (uint32_t)ns * (astage + wb + 2048) > budget) --ns;
+    p.ns = ns;
+    p.a_off = 2 * kDeqBytes;
+    p.w_off = p.a_off + ns * astage;
+    p.sz_off = p.w_off + ns * wb;
+    p.bar_off = (p.sz_off + ns * 2048 + 7) & ~7u;
+    const uint32_t smem = p.bar_off + (2 * ns + 8) * 8 + 32 + 1024;
+    if (smem > 227 * 1024) return fail(TL_EUNSUPPORTED, "tensor-core tile does not fit shared memory");
+    CUtensorMap tmap;
+    tl_status s = make_tmap_a(&tmap, A + m0 * lda, mc, K, lda, p.NB);
+    if (s != TL_OK) return s;
+    int grid = grid_req > 0 ? grid_req : sms;
+    if (grid > kTcMaxCtas) grid = kTcMaxCtas;
+    if (grid > p.units) grid = p.units;
+    s = TL_EUNSUPPORTED;
+    dispatch_format(w.kind, w.bits, w.kind == 2 ? w.exp_bits : 0, [&](auto f) {
+      using F = decltype(f);
+      s = launch_tc<F>(p, &tmap, grid, smem, st);
+    });
+    if (s != TL_OK) return s;
+  }
+  return TL_OK;
+}
+
 }  // namespace tl
