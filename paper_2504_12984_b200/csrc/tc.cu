@@ -85,14 +85,18 @@ tl_status tc_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, cons
     const uint32_t wb = (uint32_t)tile_bytes(w.bits);
     const uint32_t astage = (uint32_t)p.NB * 256;
     const uint32_t budget = 227 * 1024 - 1024 - 256;
-    int ns = 8;
-    while (ns > 2 && 2 * kDeqBytes + (uint32_t)ns * (astage + wb + 2048) > budget) --ns;
+    auto need = [&](int ns, int nd) { return (uint32_t)nd * kDeqBytes + (uint32_t)ns * (astage + wb + 2048); };
+    int ns = 8, nd = 4;
+    while (ns > 3 && need(ns, nd) > budget) --ns;
+    while (nd > 2 && need(ns, nd) > budget) --nd;
+    while (ns > 2 && need(ns, nd) > budget) --ns;
     p.ns = ns;
-    p.a_off = 2 * kDeqBytes;
+    p.nd = nd;
+    p.a_off = nd * kDeqBytes;
     p.w_off = p.a_off + ns * astage;
     p.sz_off = p.w_off + ns * wb;
     p.bar_off = (p.sz_off + ns * 2048 + 7) & ~7u;
-    const uint32_t smem = p.bar_off + (2 * ns + 8) * 8 + 32 + 1024;
+    const uint32_t smem = p.bar_off + (2 * ns + 12) * 8 + 32 + 1024;
     if (smem > 227 * 1024) return fail(TL_EUNSUPPORTED, "tensor-core tile does not fit shared memory");
     CUtensorMap tmap;
     tl_status s = make_tmap_a(&tmap, A + m0 * lda, mc, K, lda, p.NB);

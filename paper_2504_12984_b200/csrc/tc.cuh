@@ -36,6 +36,7 @@ struct TcParams {
   int NB;          // MMA N = batch tile (multiple of 16, <= 256)
   int units;       // (N/128) * (K/128)
   int ns;          // TMA ring stages
+  int nd;          // dequantized-tile ring stages (2..4)
   uint32_t a_off, w_off, sz_off, bar_off;  // smem carve-up (bytes from the 1024-aligned base)
   const uint8_t* wt;
   const __half* scales;
@@ -48,9 +49,9 @@ struct TcParams {
   uint32_t tmem_cols;
 };
 
-constexpr int kTcThreads = 320;         // 2 control warps + 8 dequant / epilogue warps
-constexpr int kTcDeqWarps = 8;
-constexpr uint32_t kDeqBytes = 128 * 128 * 2;  // one fp16 W^T tile, two 64-k swizzle blocks
+constexpr int kTcDeqWarps = 16;                 // 4 per SM sub-partition
+constexpr int kTcThreads = 64 + 32 * kTcDeqWarps;  // + TMA warp + MMA warp
+constexpr uint32_t kDeqBytes = 128 * 128 * 2;   // one fp16 W^T tile, two 64-k swizzle blocks
 
 // SWIZZLE_128B K-major UMMA shared-memory descriptor (SBO = 1024 B between 8-row atoms).
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
@@ -68,57 +69,83 @@ __device__ __forceinline__ uint32_t tc_idesc(int nb) {
   return (1u << 4) | ((uint32_t)(nb >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
 
-template <class F, int KH>
-__device__ __forceinline__ void tc_dequant_half(const uint8_t* wtile, const __half* Ss, const __half* Zs, int n,
-                                                int G, bool has_zeros, uint32_t magic, uint8_t* deq) {
+// Segment words of column c, k-quarter KQ (pairs [16*KQ, 16*KQ+16)) of a transformed tile
+// in shared memory (32-bit shared address), at the positions assemble_pair<> reads.
+template <int B, int KQ>
+__device__ __forceinline__ void load_quarter_words(uint32_t tile, int c, uint32_t* words) {
+#pragma unroll
+  for (int s = 0; s < num_segs(B); ++s) {
+    const int w = seg_width(B, s), base = seg_base(B, s);
+    const uint32_t sp = tile + 2048 * base;
+    const int j0 = w * KQ;                      // first word of this quarter
+    const uint32_t a = sp + ((j0 >> 2) * 128 + c) * 16 + (j0 & 3) * 4;
+    if (w == 1) {
+      words[4 * base + j0] = lds32(a);
+    } else if (w == 2) {
+      const uint2 x = lds64(a);
+      words[4 * base + j0] = x.x;
+      words[4 * base + j0 + 1] = x.y;
+    } else {
+#pragma unroll
+      for (int v = 0; v < w / 4; ++v) {
+        const uint4 x = lds128(a + v * 128 * 16);
+        words[4 * base + j0 + 4 * v + 0] = x.x;
+        words[4 * base + j0 + 4 * v + 1] = x.y;
+        words[4 * base + j0 + 4 * v + 2] = x.z;
+        words[4 * base + j0 + 4 * v + 3] = x.w;
+      }
+    }
+  }
+}
+
+// Dequantize pairs [16*KQ, 16*KQ+16) of row n into the 128B-swizzled K-major W^T tile:
+// 4 chunks of 8 k, logical chunk (KQ&1)*4 + j of 64-k block KQ>>1.  row_sw is the shared
+// address of (block KQ>>1, row n) XOR the row's swizzle (n&7)<<4.
+template <class F, int KQ>
+__device__ __forceinline__ void tc_dequant_quarter(uint32_t wtile, uint32_t ss, uint32_t zs, int n, bool has_zeros,
+                                                   uint32_t magic, uint32_t row_sw) {
   constexpr int B = F::bits;
   uint32_t words[4 * B];
-  load_half_words<B, KH>(wtile, n, words);
+  load_quarter_words<B, KQ>(wtile, n, words);
   PairConsts pc;
   pc.magic = magic;
-  __half2 s2 = __float2half2_rn(0.f);
+  const uint16_t sh = lds16(ss);
+  const __half2 s2 = u32_as_h2((uint32_t)sh | ((uint32_t)sh << 16));
+  float z = 0.f;
+  if constexpr (F::kind == kUint) z = has_zeros ? __half2float(__ushort_as_half(lds16(zs))) : 0.f;
+  if constexpr (F::kind == kInt) z = (float)(1 << (B - 1));
+  make_pair_consts<F>(pc, z);
   uint32_t chunk[4];
-  const int lg = G == 32 ? 5 : 6;
-  uint8_t* row = deq + KH * 16384 + n * 128;
-  const int sw = n & 7;
-  static_for<0, 32>([&](auto II) {
+  static_for<0, 16>([&](auto II) {
     constexpr int ii = decltype(II)::value;
-    constexpr int i = KH * 32 + ii;
-    if constexpr (i % 16 == 0) {
-      const int r = (G >= kBK) ? 0 : ((2 * i) >> lg);
-      const __half sh = Ss[r * kBN + n];
-      s2 = __halves2half2(sh, sh);
-      float z = 0.f;
-      if constexpr (F::kind == kUint) z = has_zeros ? __half2float(Zs[r * kBN + n]) : 0.f;
-      if constexpr (F::kind == kInt) z = (float)(1 << (B - 1));
-      make_pair_consts<F>(pc, z);
-    }
+    constexpr int i = KQ * 16 + ii;
     chunk[ii & 3] = h2_as_u32(__hmul2(pair_value<F, i>(words, pc), s2));
     if constexpr ((ii & 3) == 3) {
-      constexpr int cidx = ii >> 2;  // logical 16-byte chunk within this 64-k block
-      *reinterpret_cast<uint4*>(row + ((cidx ^ sw) << 4)) = make_uint4(chunk[0], chunk[1], chunk[2], chunk[3]);
+      constexpr uint32_t cl = (uint32_t)(((KQ & 1) * 4 + (ii >> 2)) << 4);  // logical chunk byte offset
+      sts128(row_sw ^ cl, chunk[0], chunk[1], chunk[2], chunk[3]);
     }
   });
 }
 
 template <class F>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant__ CUtensorMap tmapA, TcParams p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1024-aligned, still shared
   const int NS = p.ns;
   const int NB = p.NB;
   constexpr uint32_t WB = tile_bytes(F::bits);
   const uint32_t a_stage = (uint32_t)NB * 256;  // two 64-k boxes of NB rows x 128 B
-  uint8_t* deq = smem;                           // 2 x 32 KB
+  uint8_t* deq = smem;                           // ND x 32 KB
   uint8_t* a_s = smem + p.a_off;
   uint8_t* w_s = smem + p.w_off;
   uint8_t* sz_s = smem + p.sz_off;               // per stage: scales [4][128] + zeros [4][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bar_off);
   uint64_t* full_tma = bars;
   uint64_t* empty_tma = bars + NS;
+  const int ND = p.nd;
   uint64_t* full_deq = bars + 2 * NS;
-  uint64_t* empty_deq = full_deq + 2;
-  uint64_t* tmem_full = empty_deq + 2;
+  uint64_t* empty_deq = full_deq + 4;
+  uint64_t* tmem_full = empty_deq + 4;
   uint64_t* tmem_empty = tmem_full + 2;
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
   int* flag = reinterpret_cast<int*>(tmem_base_slot + 4);
@@ -138,9 +165,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
       mbar_init(&full_tma[s], 1);
       mbar_init(&empty_tma[s], kTcDeqWarps + 1);
     }
-    for (int d = 0; d < 2; ++d) {
+    for (int d = 0; d < ND; ++d) {
       mbar_init(&full_deq[d], kTcDeqWarps);
       mbar_init(&empty_deq[d], 1);
+    }
+    for (int d = 0; d < 2; ++d) {
       mbar_init(&tmem_full[d], 1);
       mbar_init(&tmem_empty[d], kTcDeqWarps);
     }
@@ -218,24 +247,34 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
       }
       if (++kt == KT) kt = 0;
       if (++s == NS) { s = 0; ph ^= 1; }
-      if (++d == 2) { d = 0; dph ^= 1; }
+      if (++d == ND) { d = 0; dph ^= 1; }
     }
   } else {
     // ------------------------------ dequant + epilogue ------------------------------
-    const int dw = warp - 2;             // 0..7
+    const int dw = warp - 2;             // 0..15
     const int q = warp & 3;              // TMEM lane quarter this warp may access
-    const int kh = dw >> 2;              // k-half of the tile this warp dequantizes
+    const int kq = dw >> 2;              // k-quarter of the tile this warp dequantizes
     const int n = q * 32 + lane;         // row of W^T (column of the weight / Y)
+    const uint32_t deq_u = smem_u32(deq);
+    const uint32_t w_u = smem_u32(w_s);
+    const uint32_t sz_u = smem_u32(sz_s);
+    // this thread's swizzled row address in dequant buffer 0 (block kq>>1, row n)
+    const uint32_t row_sw0 = (deq_u + (kq >> 1) * 16384 + n * 128) ^ ((uint32_t)(n & 7) << 4);
+    const int lg = p.G == 32 ? 5 : 6;
+    const int srow = (p.G >= kBK) ? 0 : ((32 * kq) >> lg);  // group row of this k-quarter in the slice
     int s = 0, ph = 0, d = 0, dph = 0, nt = u0 / KT, kt = u0 % KT, seg = 0;
     for (int u = u0; u < u1; ++u) {
       mbar_wait(&full_tma[s], ph);
-      if (u - u0 >= 2) mbar_wait(&empty_deq[d], dph ^ 1);
-      const uint8_t* wtile = w_s + s * WB;
-      const __half* Ss = reinterpret_cast<const __half*>(sz_s + s * 2048);
-      const __half* Zs = reinterpret_cast<const __half*>(sz_s + s * 2048 + 1024);
-      uint8_t* dq = deq + d * kDeqBytes;
-      if (kh == 0) tc_dequant_half<F, 0>(wtile, Ss, Zs, n, p.G, has_zeros, p.magic, dq);
-      else tc_dequant_half<F, 1>(wtile, Ss, Zs, n, p.G, has_zeros, p.magic, dq);
+      if (u - u0 >= ND) mbar_wait(&empty_deq[d], dph ^ 1);
+      const uint32_t wtile = w_u + s * WB;
+      const uint32_t ss = sz_u + s * 2048 + (srow * kBN + n) * 2;
+      const uint32_t row_sw = row_sw0 + d * kDeqBytes;
+      switch (kq) {
+        case 0: tc_dequant_quarter<F, 0>(wtile, ss, ss + 1024, n, has_zeros, p.magic, row_sw); break;
+        case 1: tc_dequant_quarter<F, 1>(wtile, ss, ss + 1024, n, has_zeros, p.magic, row_sw); break;
+        case 2: tc_dequant_quarter<F, 2>(wtile, ss, ss + 1024, n, has_zeros, p.magic, row_sw); break;
+        default: tc_dequant_quarter<F, 3>(wtile, ss, ss + 1024, n, has_zeros, p.magic, row_sw); break;
+      }
       fence_proxy_async_smem();  // make the STS visible to the tensor core (async proxy)
       __syncwarp();
       if (lane == 0) {
@@ -246,7 +285,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
       const int cur_nt = nt;
       if (++kt == KT) { kt = 0; ++nt; }
       if (++s == NS) { s = 0; ph ^= 1; }
-      if (++d == 2) { d = 0; dph ^= 1; }
+      if (++d == ND) { d = 0; dph ^= 1; }
       if (!seg_end) continue;
 
       // ---- epilogue of n-tile cur_nt (accumulator a) ----
@@ -259,7 +298,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
       const int nt_first = u0 / KT;
       const int slot = (cur_nt == nt_first) ? 0 : 1;
       float* part = p.partial + ((int64_t)(cta * 2 + slot) * NB) * kBN;
-      for (int cb = kh * 16; cb < NB; cb += 32) {
+      for (int cb = kq * 16; cb < NB; cb += 64) {
         uint32_t r[16];
         tmem_ld_32x32b_x16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * NB + cb), r);
         tmem_ld_wait();
@@ -291,7 +330,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
         if (flag[0]) {
           __threadfence();
           const int lo = flag[1], hi = flag[2];
-          for (int m = kh; m < p.M; m += 2) {
+          for (int m = kq; m < p.M; m += 4) {
             float sum = 0.f;
             for (int qq = lo; qq <= hi; ++qq) {
               const int q_first = (int)((int64_t)qq * p.units / grid) / KT;
