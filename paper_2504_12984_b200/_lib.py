@@ -53,7 +53,7 @@ def wtype(name: str) -> tl_wtype:
     return tl_wtype(2, int(m.group(3)), int(m.group(4)), int(m.group(5)))
 
 
-TL_PATH_AUTO, TL_PATH_GEMV, TL_PATH_TC = 0, 1, 2
+TL_PATH_AUTO, TL_PATH_GEMV, TL_PATH_TC, TL_PATH_TCS = 0, 1, 2, 3
 
 _c_size = ctypes.c_size_t
 _i64 = ctypes.c_int64

@@ -29,12 +29,13 @@ static int env_int(const char* name, int dflt) {
 // Path choice (row a2).  PAPER.md:546 used CUDA cores for 1-15 tokens and tensor
 // cores from 16 on an L40S; on B200 the crossover is lower and is set
 // from the measured sweep.
-static int choose_path(tl_wtype w, int64_t M) {
+static int choose_path(tl_wtype w, int64_t M, int32_t G) {
   const int forced = env_int("TL_FORCE_PATH", 0);
-  if (forced == TL_PATH_GEMV || forced == TL_PATH_TC) return forced;
+  if (forced == TL_PATH_GEMV || forced == TL_PATH_TC || forced == TL_PATH_TCS) return forced;
   if (!tc_available()) return TL_PATH_GEMV;
   (void)w;
-  // measured on B200: the CUDA-core path wins only at M = 1
+  // measured on B200
+  if (tcs_eligible(M, G)) return TL_PATH_TCS;
   return M <= 1 ? TL_PATH_GEMV : TL_PATH_TC;
 }
 
@@ -68,6 +69,8 @@ size_t tl_matmul_workspace_bytes(tl_wtype w, int64_t M, int64_t N, int64_t K, in
   if (M <= 0 || N <= 0 || K <= 0) return kSemBytes;
   size_t g = gemv_workspace_bytes(M, N, K);
   size_t t = tc_workspace_bytes(M, N, K);
+  size_t ts = tcs_workspace_bytes(M, N, K);
+  if (ts > t) t = ts;
   return kSemBytes + (g > t ? g : t);
 }
 
@@ -76,7 +79,7 @@ tl_status tl_matmul_plan(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t gr
   (void)N;
   (void)K;
   (void)group;
-  if (path_out) *path_out = choose_path(w, M);
+  if (path_out) *path_out = choose_path(w, M, group);
   if (splits_out) *splits_out = 0;
   return TL_OK;
 }
@@ -101,7 +104,8 @@ tl_status tl_matmul_ex(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t grou
   if (!workspace || workspace_bytes < need)
     return fail(TL_EWORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
   if (!aligned16(workspace)) return fail(TL_EALIGN, "workspace must be 16-byte aligned");
-  if (path == TL_PATH_AUTO) path = choose_path(w, M);
+  if (path == TL_PATH_AUTO) path = choose_path(w, M, group);
+  if (path == TL_PATH_TCS && !tcs_eligible(M, group)) path = TL_PATH_TC;
   int* sem = reinterpret_cast<int*>(workspace);
   float* partial = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(workspace) + kSemBytes);
   cudaStream_t s = as_stream(stream);
@@ -141,6 +145,12 @@ tl_status tl_matmul_ex(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t grou
                      reinterpret_cast<const uint8_t*>(w_t), reinterpret_cast<const __half*>(scales),
                      reinterpret_cast<const __half*>(zeros), reinterpret_cast<__half*>(Y), ldy, partial, sem,
                      splits, s);
+  }
+  if (path == TL_PATH_TCS) {
+    return tcs_matmul(w, M, N, K, group, reinterpret_cast<const __half*>(A), lda,
+                      reinterpret_cast<const uint8_t*>(w_t), reinterpret_cast<const __half*>(scales),
+                      reinterpret_cast<const __half*>(zeros), reinterpret_cast<__half*>(Y), ldy, partial, sem,
+                      splits, s);
   }
   return fail(TL_EUNSUPPORTED, "unknown path %d", path);
 }

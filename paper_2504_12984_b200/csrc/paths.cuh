@@ -29,5 +29,10 @@ size_t tc_workspace_bytes(int64_t M, int64_t N, int64_t K);
 tl_status tc_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, const __half* A, int64_t lda,
                     const uint8_t* wt, const __half* scales, const __half* zeros, __half* Y, int64_t ldy,
                     float* partial, int* sem, int grid_req, cudaStream_t st);
+bool tcs_eligible(int64_t M, int32_t G);
+size_t tcs_workspace_bytes(int64_t M, int64_t N, int64_t K);
+tl_status tcs_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, const __half* A, int64_t lda,
+                     const uint8_t* wt, const __half* scales, const __half* zeros, __half* Y, int64_t ldy,
+                     float* partial, int* sem, int grid_req, cudaStream_t st);
 
 }  // namespace tl

@@ -226,13 +226,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
       mbar_wait(&full_tma[s], ph);
       tc_fence_after();
       if (elect_one()) {
-        const uint32_t a_base = smem_u32(deq + d * kDeqBytes);
-        const uint32_t b_base = smem_u32(a_s + s * a_stage);
+        // descriptors advance 32 B per k-step inside a 64-k block (+2 in 16-B units); the W^T
+        // tile's second block is 16 KB on (+1024), the activation tile's NB*128 B on
+        const uint64_t ad0 = sw128_desc(smem_u32(deq + d * kDeqBytes));
+        const uint64_t bd0 = sw128_desc(smem_u32(a_s + s * a_stage));
         const uint32_t dt = tmem + (uint32_t)(a * NB);
+        const uint32_t bblk = (uint32_t)NB * 8;  // NB*128 B in 16-B units
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const uint64_t ad = sw128_desc(a_base + (j >> 2) * 16384 + (j & 3) * 32);
-          const uint64_t bd = sw128_desc(b_base + (j >> 2) * (NB * 128) + (j & 3) * 32);
+          const uint64_t ad = ad0 + (uint64_t)((j >> 2) * 1024 + (j & 3) * 2);
+          const uint64_t bd = bd0 + (uint64_t)((j >> 2) * bblk + (j & 3) * 2);
           tc_mma_f16_ss(dt, ad, bd, idesc, (first && j == 0) ? 0u : 1u);
         }
         tc_commit(&empty_deq[d]);
