@@ -57,10 +57,10 @@ tl_status tcs_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, con
     p.trace = g_trace;
   }
   const uint32_t stage = (uint32_t)tile_bytes(w.bits);
-  const uint32_t red = 4u * (uint32_t)M * kBN * 4;
+  const uint32_t red = (uint32_t)kTcsGroups * (uint32_t)M * kBN * 4;
   const uint32_t budget = 227 * 1024 - 1024 - 512;
   int ns = 32, lg = 5;
-  while (ns > 2 && 4 * kTcsApBytes + (uint32_t)ns * stage + red > budget) {
+  while (ns > 2 && kTcsWSlots * kTcsApBytes + (uint32_t)ns * stage + red + 16 * kTcsNB * 16 + 1024 > budget) {
     ns >>= 1;
     --lg;
   }
@@ -68,10 +68,10 @@ tl_status tcs_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, con
   p.lg_ns = lg;
   p.stage_bytes = stage;
   p.ap_off = 0;
-  p.st_off = 4 * kTcsApBytes;
+  p.st_off = kTcsWSlots * kTcsApBytes;
   p.red_off = p.st_off + ns * stage;
-  p.bar_off = (p.red_off + red + 7) & ~7u;
-  const uint32_t smem = p.bar_off + (2 * ns + 24) * 8 + 16 * kTcsNB * 4 + 32 + 1024;
+  p.bar_off = (p.red_off + red + 15) & ~15u;
+  const uint32_t smem = p.bar_off + (2 * ns + 2 * kTcsWSlots + 16) * 8 + 16 * kTcsNB * 16 + 32 + 1024;
   if (smem > 227 * 1024) return fail(TL_EUNSUPPORTED, "decode tensor-core tile does not fit shared memory");
   int grid = grid_req > 0 ? grid_req : sms;
   if (grid > 160) grid = 160;

@@ -51,12 +51,13 @@ struct TcsParams {
   long long* trace;  // optional [5][256] clock64 stamps of CTA 0 (debug)
 };
 
-constexpr int kTcsGroups = 4;
+constexpr int kTcsGroups = 3;        // dequant groups; each owns 2 TMEM W^T slots
 constexpr int kTcsThreads = 64 + kTcsGroups * 128;
 constexpr int kTcsNB = 16;
 constexpr uint32_t kTcsApBytes = kTcsNB * 256;  // activation operand tile (16 rows x 128 k fp16)
-// TMEM columns: W^T slots [0,256) (4 x 64), accumulators [256,384) (8 x 16)
-constexpr uint32_t kTcsAccCol = 256;
+constexpr int kTcsWSlots = 2 * kTcsGroups;        // W^T tiles in TMEM (64 columns each)
+// TMEM columns: W^T slots [0,384) (6 x 64), accumulators [384,512) (8 x 16)
+constexpr uint32_t kTcsAccCol = 64 * kTcsWSlots;
 
 template <int B, int I>
 struct SubP {  // bit position of pair I's code in each 16-bit half (same rule as PairP)
@@ -156,12 +157,12 @@ __global__ void __launch_bounds__(kTcsThreads, 1) tcs_kernel(TcsParams p) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bar_off);
   uint64_t* full_tma = bars;
   uint64_t* empty_tma = bars + NS;
-  uint64_t* full_w = bars + 2 * NS;     // [4]  W^T slot g written by group g
-  uint64_t* empty_w = full_w + 4;       // [4]  MMA done with W^T slot g
-  uint64_t* full_acc = empty_w + 4;     // [8]  accumulator slot t&7 ready
+  uint64_t* full_w = bars + 2 * NS;     // [6]  W^T slot written by its group
+  uint64_t* empty_w = full_w + kTcsWSlots;  // [6]  MMA done with W^T slot
+  uint64_t* full_acc = empty_w + kTcsWSlots;  // [8]  accumulator slot t&7 ready
   uint64_t* empty_acc = full_acc + 8;   // [8]  accumulator slot read back
-  float* asum = reinterpret_cast<float*>(empty_acc + 8);  // [16][16] sum_k A[m,k] of tile t&15
-  uint32_t* tslot_ptr = reinterpret_cast<uint32_t*>(asum + 16 * kTcsNB);
+  float* asum = reinterpret_cast<float*>(empty_acc + 8);  // [16][16][4] per-warp sum_k A[m,k] of tile t&15
+  uint32_t* tslot_ptr = reinterpret_cast<uint32_t*>(asum + 16 * kTcsNB * 4);
   int* flag = reinterpret_cast<int*>(tslot_ptr + 4);
 
   const int KT = p.K / kBK;
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(kTcsThreads, 1) tcs_kernel(TcsParams p) {
       mbar_init(&full_tma[s], 1);
       mbar_init(&empty_tma[s], 4);
     }
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < kTcsWSlots; ++i) {
       mbar_init(&full_w[i], 4);
       mbar_init(&empty_w[i], 1);
     }
@@ -194,7 +195,7 @@ __global__ void __launch_bounds__(kTcsThreads, 1) tcs_kernel(TcsParams p) {
     tmem_relinquish();
   }
   // zero the activation operand tiles (rows >= M stay zero)
-  for (uint32_t i = threadIdx.x; i < 4 * kTcsApBytes / 16; i += kTcsThreads)
+  for (uint32_t i = threadIdx.x; i < kTcsWSlots * kTcsApBytes / 16; i += kTcsThreads)
     sts128(smem_u32(ap) + i * 16, 0u, 0u, 0u, 0u);
   fence_proxy_async_smem();
   tc_fence_before();
@@ -220,8 +221,10 @@ __global__ void __launch_bounds__(kTcsThreads, 1) tcs_kernel(TcsParams p) {
       const uint32_t idesc = (1u << 4) | ((uint32_t)(kTcsNB >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
       const uint64_t bd_base = sw128_desc_s(smem_u32(ap));
       for (int t = 0; t < T; ++t) {
-        const int ws = t & 3, as = t & 7;
-        mbar_wait(&full_w[ws], (t >> 2) & 1);
+        // tile t belongs to group t%3; its k-th tile (k = t/3) uses W^T slot 2g + (k&1)
+        const int gk = t / kTcsGroups, gg = t - gk * kTcsGroups;
+        const int ws = 2 * gg + (gk & 1), as = t & 7;
+        mbar_wait(&full_w[ws], (gk >> 1) & 1);
         tcs_stamp(p, 7, t);
         if (t >= 8) mbar_wait(&empty_acc[as], ((t >> 3) - 1) & 1);
         tc_fence_after();
@@ -241,48 +244,47 @@ __global__ void __launch_bounds__(kTcsThreads, 1) tcs_kernel(TcsParams p) {
     }
   } else {
     // ------------------------------ dequant groups ------------------------------
-    const int dw = warp - 2;            // 0..15
+    const int dw = warp - 2;            // 0..11
     const int g = dw >> 2;              // dequant group
     const int q = warp & 3;             // TMEM lane quarter
     const int n = q * 32 + lane;        // row of W^T = output column within the n-tile
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    const uint32_t tslot = tmem + lane_off + g * 64;
-    const uint32_t ap_u = smem_u32(ap + g * kTcsApBytes);
     const uint32_t st_u = smem_u32(st);
-    // activation conversion: lane L handles k = 4L..4L+3 (pairs 2L, 2L+1) of rows m = q + 4j
+    // activation conversion: lane L of warp q handles the 4 k of chunk c = 8q + (L&7)
+    // (pairs 2c, 2c+1) of rows m = (L>>3) + 4j, so every warp shares the work at any M
+    const int ac = q * 8 + (lane & 7);
+    const int ar0 = lane >> 3;
     float pre0 = 1.f, pre1 = 1.f;  // 2^-P for the lane's two pairs (ints); 1 for floats
     if constexpr (kD2) {
       int P0 = 0, P1 = 0;
       static_for<0, 64>([&](auto II) {
         constexpr int i = decltype(II)::value;
-        if (i == 2 * lane) P0 = SubP<F::bits, i>::value;
-        if (i == 2 * lane + 1) P1 = SubP<F::bits, i>::value;
+        if (i == 2 * ac) P0 = SubP<F::bits, i>::value;
+        if (i == 2 * ac + 1) P1 = SubP<F::bits, i>::value;
       });
       pre0 = __int_as_float((127 - P0) << 23);
       pre1 = __int_as_float((127 - P1) << 23);
     }
     const __half2 pre0h = __float2half2_rn(pre0), pre1h = __float2half2_rn(pre1);
-    const uint32_t a_kb = (uint32_t)(lane >> 4) * (kTcsNB * 128);   // 64-k block
-    const uint32_t a_c = (uint32_t)((lane & 15) >> 1);              // 16-byte chunk in the row
-    const uint32_t a_h = (uint32_t)(lane & 1) * 8;                  // half of the chunk
+    const uint32_t a_kb = (uint32_t)(ac >> 4) * (kTcsNB * 128);   // 64-k block
+    const uint32_t a_c = (uint32_t)((ac & 15) >> 1);              // 16-byte chunk in the row
+    const uint32_t a_h = (uint32_t)(ac & 1) * 8;                  // half of the chunk
     const float c1mul = kD2 ? 16777216.f : (float)(1 << (15 - F::bias));
     constexpr int RJ = (MT + 3) / 4;  // activation rows per warp
     float tot[MT];
 #pragma unroll
     for (int m = 0; m < MT; ++m) tot[m] = 0.f;
 
-    auto load_a = [&](int t, uint2 (&ar)[RJ]) {
-      const int u = u0 + t, kt_ = u % KT;
+    auto load_a = [&](int kt_, uint2 (&ar)[RJ]) {
 #pragma unroll
       for (int j = 0; j < RJ; ++j) {
-        const int m = q + 4 * j;
+        const int m = ar0 + 4 * j;
         if (m < p.M)
-          ar[j] = __ldg(reinterpret_cast<const uint2*>(p.A + (int64_t)m * p.lda + (int64_t)kt_ * kBK + lane * 4));
+          ar[j] = __ldg(reinterpret_cast<const uint2*>(p.A + (int64_t)m * p.lda + (int64_t)kt_ * kBK + ac * 4));
       }
     };
     // raw fp16 bits; converted only in the (lagged) fixup so the load latency is never waited on
-    auto load_sz = [&](int t, uint16_t& sc_, uint16_t& z_) {
-      const int u = u0 + t, nt_ = u / KT, kt_ = u - nt_ * KT;
+    auto load_sz = [&](int nt_, int kt_, uint16_t& sc_, uint16_t& z_) {
       const int gg = (int)((int64_t)kt_ * kBK / p.G);
       const int64_t off = (int64_t)gg * p.N + nt_ * kBN + n;
       sc_ = __ldg(reinterpret_cast<const unsigned short*>(p.scales) + off);
@@ -308,20 +310,29 @@ __global__ void __launch_bounds__(kTcsThreads, 1) tcs_kernel(TcsParams p) {
       if (lane == 0) mbar_arrive(&empty_acc[as]);
       if (lane == 0 && q == 2) tcs_stamp(p, 4, tp);
       const float c1 = sc_ * c1mul, c2 = -sc_ * z_;
-      const float* as_m = asum + (tp & 15) * kTcsNB;
+      const float* as_m = asum + (tp & 15) * kTcsNB * 4;
 #pragma unroll
       for (int m = 0; m < MT; ++m) {
         if (m < p.M) {
           float v = tot[m];
-          if constexpr (kD2) v = fmaf(c2, as_m[m], v);
+          if constexpr (kD2) {
+            const float4 a4 = *reinterpret_cast<const float4*>(as_m + m * 4);  // 4 warps' partial sums
+            v = fmaf(c2, (a4.x + a4.y) + (a4.z + a4.w), v);
+          }
           tot[m] = fmaf(c1, __uint_as_float(d[m]), v);
         }
       }
+      if (lane == 0 && q == 2) tcs_stamp(p, 8, tp);
     };
 
     uint2 araw_n[RJ];
     int t = g;
-    if (t < T) load_a(t, araw_n);
+    int kk = 0;                  // this group's tile counter (t = g + 3*kk)
+    // (n-tile, k-tile) of this group's current tile and of the next one, tracked incrementally
+    int nt_c = (u0 + t) / KT, kt_c = (u0 + t) - ((u0 + t) / KT) * KT;
+    int nt_n = nt_c, kt_n = kt_c + kTcsGroups;
+    while (kt_n >= KT) { kt_n -= KT; ++nt_n; }
+    if (t < T) load_a(kt_c, araw_n);
     int tp = -1;                 // this group's tile whose fixup is pending
     uint16_t sc_p = 0, z_p = 0;  // its scale / zero (fp16 bits)
     int t0 = 0;
@@ -329,50 +340,65 @@ __global__ void __launch_bounds__(kTcsThreads, 1) tcs_kernel(TcsParams p) {
       const int ufirst = u0 + t0;
       const int nt = ufirst / KT;
       const int t1 = min(T, t0 + (KT - (ufirst - nt * KT)));
-      for (; t < t1; t += 4) {
+      for (; t < t1; t += kTcsGroups, ++kk) {
+        if (lane == 0 && q == 2) tcs_stamp(p, 9, t);
+        const int ws = 2 * g + (kk & 1);
+        const uint32_t tslot = tmem + lane_off + ws * 64;
+        const uint32_t ap_u = smem_u32(ap + ws * kTcsApBytes);
         uint2 araw[RJ];
 #pragma unroll
         for (int j = 0; j < RJ; ++j) araw[j] = araw_n[j];
-        if (t + 4 < T) load_a(t + 4, araw_n);
+        if (t + kTcsGroups < T) load_a(kt_n, araw_n);
         uint16_t sc_c, z_c;
-        load_sz(t, sc_c, z_c);           // consumed by this tile's (lagged) fixup
+        load_sz(nt_c, kt_c, sc_c, z_c);  // consumed by this tile's (lagged) fixup
+        nt_c = nt_n;
+        kt_c = kt_n;
+        kt_n += kTcsGroups;
+        while (kt_n >= KT) { kt_n -= KT; ++nt_n; }
         const int s = t & (NS - 1);
+        if (lane == 0 && q == 2) tcs_stamp(p, 10, t);
         mbar_wait(&full_tma[s], (t >> p.lg_ns) & 1);
-        if (t >= 4) mbar_wait(&empty_w[g], ((t >> 2) - 1) & 1);
+        if (lane == 0 && q == 2) tcs_stamp(p, 11, t);
+        if (kk >= 2) mbar_wait(&empty_w[ws], ((kk >> 1) - 1) & 1);
         if (lane == 0 && q == 2) tcs_stamp(p, 2, t);
-        if (lane == 0) tcs_stamp(p, 12 + q, t);
         uint32_t words[4 * F::bits];
         tcs_load_words<F::bits>(st_u + s * stage_bytes, n, words);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_tma[s]);   // the stage goes back to the TMA ring now
         tcs_dequant_tile<F>(words, tslot);
-        // activation operand (rows m = q + 4j < M, prescaled by 2^-P) and its row sums
+        // activation operand (prescaled by 2^-P) and the per-warp partial row sums
 #pragma unroll
         for (int j = 0; j < RJ; ++j) {
-          const int m = q + 4 * j;
-          if (m < p.M) {
-            __half2 a0 = u32_as_h2(araw[j].x), a1 = u32_as_h2(araw[j].y);
+          const int m = ar0 + 4 * j;
+          if (j * 4 < p.M) {           // warp-uniform: every lane takes part in the shuffles
+            __half2 a0 = u32_as_h2(0u), a1 = u32_as_h2(0u);
+            if (m < p.M) {
+              a0 = u32_as_h2(araw[j].x);
+              a1 = u32_as_h2(araw[j].y);
+            }
             if constexpr (kD2) {
               const float2 f0 = __half22float2(a0), f1 = __half22float2(a1);
               float sum = (f0.x + f0.y) + (f1.x + f1.y);
-#pragma unroll
-              for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-              if (lane == 0) asum[(t & 15) * kTcsNB + m] = sum;
+              sum += __shfl_xor_sync(0xffffffffu, sum, 4);
+              sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+              sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+              if ((lane & 7) == 0 && m < p.M) asum[((t & 15) * kTcsNB + m) * 4 + q] = sum;
               a0 = __hmul2(a0, pre0h);
               a1 = __hmul2(a1, pre1h);
             }
-            const uint32_t dst = ap_u + a_kb + m * 128 + (((a_c ^ (uint32_t)(m & 7))) << 4) + a_h;
-            asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(dst), "r"(h2_as_u32(a0)), "r"(h2_as_u32(a1))
-                         : "memory");
+            if (m < p.M) {
+              const uint32_t dst = ap_u + a_kb + m * 128 + (((a_c ^ (uint32_t)(m & 7))) << 4) + a_h;
+              asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(dst), "r"(h2_as_u32(a0)), "r"(h2_as_u32(a1))
+                           : "memory");
+            }
           }
         }
         tmem_st_wait();
         fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&full_w[g]);
+        if (lane == 0) mbar_arrive(&full_w[ws]);
         if (lane == 0 && q == 2) tcs_stamp(p, 3, t);
-        if (lane == 0) tcs_stamp(p, 8 + q, t);
         if (tp >= 0) {
           named_bar_sync(2 + g, 128);   // this group's row sums of tile tp are visible
           fixup(tp, sc_p, z_p);
@@ -397,9 +423,9 @@ __global__ void __launch_bounds__(kTcsThreads, 1) tcs_kernel(TcsParams p) {
       const int col = nt * kBN + n;
       const int slot2 = (nt == u0 / KT) ? 0 : 1;
       float* part = p.partial + ((int64_t)(cta * 2 + slot2) * kTcsNB) * kBN;
-      for (int m = g; m < p.M; m += 4) {
+      for (int m = g; m < p.M; m += kTcsGroups) {
         const float v = red[(0 * p.M + m) * kBN + n] + red[(1 * p.M + m) * kBN + n] +
-                        red[(2 * p.M + m) * kBN + n] + red[(3 * p.M + m) * kBN + n];
+                        red[(2 * p.M + m) * kBN + n];
         if (complete) p.Y[(int64_t)m * p.ldy + col] = __float2half_rn(v);
         else __stcg(part + (int64_t)m * kBN + n, v);
       }
@@ -418,7 +444,7 @@ __global__ void __launch_bounds__(kTcsThreads, 1) tcs_kernel(TcsParams p) {
         if (flag[0]) {
           __threadfence();
           const int lo = flag[1], hi = flag[2];
-          for (int m = g; m < p.M; m += 4) {
+          for (int m = g; m < p.M; m += kTcsGroups) {
             float sum = 0.f;
             for (int qq = lo; qq <= hi; ++qq) {
               const int q_first = (int)((int64_t)qq * p.units / grid) / KT;

@@ -16,7 +16,7 @@ buf = (ctypes.c_longlong * (16 * 256))()
 P._lib._lib.tl__debug_trace(buf)
 a = np.array(buf, dtype=np.int64).reshape(16, 256)
 t0 = a[0, 0]
-names = ["prod", "mma_go", "deq_st", "deq_dn", "acc_rdy", "mma_iss", "mma_com", "mma_fw", "dn_q0", "dn_q1", "dn_q2", "dn_q3", "st_q0", "st_q1", "st_q2", "st_q3"]
+names = ["prod", "mma_go", "deq_st", "deq_dn", "fx_acc", "mma_iss", "mma_com", "mma_fw", "fx_end", "top", "pre_w", "tma_ok", "-", "-", "-", "-"]
 print("tile " + " ".join(f"{n:>7s}" for n in names))
 for t in range(0, 64):
     print(f"{t:4d} " + " ".join(f"{(a[k, t] - t0):7d}" for k in range(16)))
