@@ -176,6 +176,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_2504_12984_b200 as P
+    from paper_2504_12984_b200.dist import gather_columns
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -211,7 +212,6 @@ def run_ours(args):
         for p in probs:
             p["A"] = wl.gen_activations_torch(m, p["K"], wl.stable_seed("A", p["layer"], m, rank), dev)
             p["Y"] = torch.empty((m, p["N"]), dtype=torch.float16, device=dev)
-            p["Yg"] = torch.empty((world, m, p["N"]), dtype=torch.float16, device=dev) if args.gather else None
 
     def step(m, events=None):
         for i, p in enumerate(probs):
@@ -221,7 +221,7 @@ def run_ours(args):
             if events is not None:
                 events[i][1].record(stream)
             if args.gather:
-                dist.all_gather_into_tensor(p["Yg"], p["Y"])
+                gather_columns(p["Y"], world * p["N"], world)
 
     def timed(m, steps, warmup, per_launch=True, sampler=None):
         make_io(m)

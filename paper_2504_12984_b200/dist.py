@@ -1,0 +1,86 @@
+"""Column (N) sharding of the A16Wx matmul across the GPUs of one box.
+
+Output column n depends only on W[:, n], s[:, n], z[:, n] and all of A (the paper's
+independent output tiles), so a column shard needs no communication
+to compute.  Rank r owns columns [n0, n1) = column_shard(N, world, r): contiguous,
+multiples of 128 (the transformed layout's tile width).  Each rank transforms its own
+shard once (tl_transform_weights) and runs tl_matmul on it; only the *gathered* variant
+exchanges data: one all-gather of the Y shards (NCCL over NVLink on B200; any
+torch.distributed backend works, the CPU tests use gloo).
+
+This module holds shard arithmetic and the collective only; every matmul runs in the
+CUDA library through ``_lib``.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import _lib as L
+
+TILE = 128
+
+
+def column_shard(N: int, world: int, rank: int, align: int = TILE) -> tuple[int, int]:
+    """Columns [n0, n1) of rank `rank`: contiguous, `align`-multiples, sizes differ by <= align."""
+    if N % align:
+        raise ValueError(f"N={N} is not a multiple of {align}")
+    if not 0 <= rank < world:
+        raise ValueError("bad rank")
+    tiles = N // align
+    t0 = rank * tiles // world
+    t1 = (rank + 1) * tiles // world
+    return t0 * align, t1 * align
+
+
+def gather_columns(Y_shard: torch.Tensor, N: int, world: int, group=None) -> torch.Tensor:
+    """All-gather the [M, n1-n0] shards of every rank into Y [M, N] (column order by rank).
+
+    Shards must have equal width (N divisible by world*128) so all_gather_into_tensor can
+    be used; the result is a [world, M, Ns] buffer viewed/permuted to [M, N].
+    """
+    M, Ns = Y_shard.shape
+    if Ns * world != N:
+        raise ValueError("gather_columns needs equal shard widths (N % (world*128) == 0)")
+    buf = torch.empty((world * M, Ns), dtype=Y_shard.dtype, device=Y_shard.device)
+    dist.all_gather_into_tensor(buf, Y_shard.contiguous(), group=group)
+    buf = buf.view(world, M, Ns)
+    if M == 1:
+        return buf.view(1, N)            # rank-major columns are already contiguous
+    return buf.permute(1, 0, 2).reshape(M, N)
+
+
+class ShardedA16WxLinear:
+    """One rank's column shard of an A16Wx linear layer Y = A x dequant(W)."""
+
+    def __init__(self, fmt: str, K: int, N: int, group: int, codes_shard: torch.Tensor, scales_shard: torch.Tensor,
+                 zeros_shard: torch.Tensor | None, world: int, rank: int, pg=None):
+        self.w = L.wtype(fmt)
+        self.K, self.N, self.G = K, N, group
+        self.world, self.rank, self.pg = world, rank, pg
+        self.n0, self.n1 = column_shard(N, world, rank)
+        Ns = self.n1 - self.n0
+        if tuple(codes_shard.shape) != (K, Ns):
+            raise ValueError("codes_shard must be [K, n1-n0]")
+        bs = L.tl_pack(self.w, K, Ns, codes_shard.contiguous())
+        self.w_t = L.tl_transform_weights(self.w, K, Ns, bs)
+        self.scales = scales_shard.contiguous()
+        self.zeros = None if zeros_shard is None else zeros_shard.contiguous()
+        self.Ns = Ns
+        self._ws = {}
+
+    def _workspace(self, M: int) -> torch.Tensor:
+        if M not in self._ws:
+            self._ws[M] = L.alloc_workspace(self.w, M, self.Ns, self.K, self.G, device=self.w_t.device)
+        return self._ws[M]
+
+    def forward(self, A: torch.Tensor, gather: bool = False, out: torch.Tensor | None = None) -> torch.Tensor:
+        M = A.shape[0]
+        Y = out if out is not None else torch.empty((M, self.Ns), dtype=torch.float16, device=A.device)
+        L.tl_matmul(self.w, M, self.Ns, self.K, self.G, A, self.w_t, self.scales, self.zeros, Y, self._workspace(M))
+        if not gather:
+            return Y
+        return gather_columns(Y, self.N, self.world, self.pg)
+
+    __call__ = forward

@@ -1,0 +1,83 @@
+"""Host logic of the N-sharded multi-GPU path on CPU with world_size-2 gloo.
+
+Each rank computes its column shard with the oracle (the CPU stand-in for tl_matmul on
+its GPU), gather_columns reassembles Y, and the result must equal the full oracle output
+bit for bit (column independence)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import workloads as wl
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _column_shard(N, world, rank):
+    # imported lazily inside the worker so the spawn start-up stays light
+    from paper_2504_12984_b200.dist import column_shard
+    return column_shard(N, world, rank)
+
+
+def _worker(rank, world, port, fmt, M, K, N, G, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import dequant, matmul_fp64, parse_wtype
+    from paper_2504_12984_b200.dist import column_shard, gather_columns
+    seed = wl.stable_seed("dist", fmt, M, K, N)
+    A = wl.gen_activations(M, K, seed)
+    codes = wl.gen_codes(fmt, K, N, seed)
+    s = wl.gen_scales(fmt, K, N, G, seed)
+    z = wl.gen_zeros(fmt, K, N, G, seed)
+    n0, n1 = column_shard(N, world, rank)
+    w = dequant(parse_wtype(fmt), codes[:, n0:n1], s[:, n0:n1], None if z is None else z[:, n0:n1], G)
+    y_shard = torch.from_numpy(matmul_fp64(A, w).astype(np.float16))
+    Y = gather_columns(y_shard, N, world)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "Y.npy"), Y.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("M", [1, 3])
+def test_gather_two_ranks_matches_full_oracle(tmp_path, M):
+    world, fmt, K, N, G = 2, "u4", 256, 1024, 128
+    mp.spawn(_worker, args=(world, _free_port(), fmt, M, K, N, G, str(tmp_path)), nprocs=world, join=True)
+    Y = np.load(tmp_path / "Y.npy")
+    from oracle import dequant, matmul_fp64, parse_wtype
+    seed = wl.stable_seed("dist", fmt, M, K, N)
+    A = wl.gen_activations(M, K, seed)
+    full = matmul_fp64(A, dequant(parse_wtype(fmt), wl.gen_codes(fmt, K, N, seed), wl.gen_scales(fmt, K, N, G, seed),
+                                  wl.gen_zeros(fmt, K, N, G, seed), G)).astype(np.float16)
+    assert np.array_equal(Y.view(np.uint16), full.view(np.uint16))
+
+
+@pytest.mark.parametrize("N,world", [(57344, 8), (57344, 2), (1024, 8), (384, 2), (10240, 8), (640, 3)])
+def test_column_shards_partition_and_align(N, world):
+    spans = [_column_shard(N, world, r) for r in range(world)]
+    assert spans[0][0] == 0 and spans[-1][1] == N
+    for (a, b), (c, d) in zip(spans, spans[1:]):
+        assert b == c
+    widths = [b - a for a, b in spans]
+    assert all(w % 128 == 0 and w > 0 for w in widths)
+    assert max(widths) - min(widths) <= 128
+
+
+def test_column_shard_rejects_bad_inputs():
+    from paper_2504_12984_b200.dist import column_shard
+    with pytest.raises(ValueError):
+        column_shard(1000, 2, 0)
+    with pytest.raises(ValueError):
+        column_shard(1024, 2, 2)
