@@ -71,7 +71,7 @@ tl_status tcs_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, con
   p.st_off = kTcsWSlots * kTcsApBytes;
   p.red_off = p.st_off + ns * stage;
   p.bar_off = (p.red_off + red + 15) & ~15u;
-  const uint32_t smem = p.bar_off + (2 * ns + 2 * kTcsWSlots + 16) * 8 + 16 * kTcsNB * 16 + 32 + 1024;
+  const uint32_t smem = p.bar_off + (2 * ns + 2 * kTcsWSlots + 16) * 8 + 32 + 1024;
   if (smem > 227 * 1024) return fail(TL_EUNSUPPORTED, "decode tensor-core tile does not fit shared memory");
   int grid = grid_req > 0 ? grid_req : sms;
   if (grid > 160) grid = 160;

@@ -9,10 +9,9 @@
 //    16-bit half ARE the fp16 subnormal u * 2^(P-24) (exact -- fp16 subnormals are multiplied
 //    exactly by the tensor core, checked by tools/tc_probe.cu), and the activation operand is
 //    pre-scaled by 2^-P per k, so the MMA accumulates 2^-24 * sum_k A[m,k] u[k,n] in fp32;
-//  * the zero point and the group scale are applied once per (128-k tile, batch row) in fp32
-//    from TMEM, with the activation row sums S = sum_k A[m,k] of the tile computed while the
-//    activation operand is built: Y += s * (2^24 * D - z * S)  (int codes are stored
-//    offset-binary, so ints use z = 2^(b-1));
+//  * the zero point is removed with one exact HSUB2 per pair ((u - z) * 2^(P-24) is still an
+//    exact fp16), and the group scale is applied once per (128-k tile, batch row) in fp32 from
+//    TMEM: Y += s * 2^24 * D  (int codes are stored offset-binary, so ints use z = 2^(b-1));
 //    float codes are placed on the fp16 exponent/mantissa fields (value * 2^(bias-15), exact)
 //    and Y += s * 2^(15-bias) * D.  Every product is exact; sums are fp32.
 //
@@ -125,17 +124,35 @@ __device__ __forceinline__ void tcs_load_words(uint32_t wtile, int n, uint32_t* 
 }
 
 // One 128x128 tile: row n's 64 pairs -> TMEM slot (4 x tcgen05.st of 16 columns).
+// ints: the raw pair is (u * 2^(P-24)) in fp16 (subnormal or small normal, exact); one HSUB2
+// with the row's constant z * 2^(P-24) leaves (u - z) * 2^(P-24), still exact, so the zero point
+// needs no correction term later.  floats: the raw pair is value * 2^(bias-15), exact.
 template <class F>
-__device__ __forceinline__ void tcs_dequant_tile(const uint32_t* words, uint32_t tslot) {
+__device__ __forceinline__ void tcs_dequant_tile(const uint32_t* words, uint32_t tslot, const uint32_t (&cz)[11]) {
   static_for<0, 4>([&](auto CC) {
     constexpr int c = decltype(CC)::value;
     uint32_t r[16];
     static_for<0, 16>([&](auto II) {
       constexpr int ii = decltype(II)::value;
-      r[ii] = tcs_pair_bits<F, c * 16 + ii>(words);
+      constexpr int i = c * 16 + ii;
+      const uint32_t x = tcs_pair_bits<F, i>(words);
+      if constexpr (F::kind != kFloat) r[ii] = h2_as_u32(__hsub2(u32_as_h2(x), u32_as_h2(cz[SubP<F::bits, i>::value])));
+      else r[ii] = x;
     });
     tmem_st_32x32b_x16(tslot + c * 16, r);
   });
+}
+
+// z * 2^(P-24) as fp16x2 for every P a pair of a b-bit code can sit at
+template <class F>
+__device__ __forceinline__ void tcs_zero_consts(float z, uint32_t (&cz)[11]) {
+#pragma unroll
+  for (int P = 0; P <= 10; ++P) {
+    if (pair_p_used<F::bits>(P)) {
+      const __half h = __float2half_rn(z * __int_as_float((127 + P - 24) << 23));
+      cz[P] = h2_as_u32(__halves2half2(h, h));
+    }
+  }
 }
 
 __device__ __forceinline__ void tcs_stamp(const TcsParams& p, int kind, int t) {
@@ -161,8 +178,7 @@ __global__ void __launch_bounds__(kTcsThreads, 1) tcs_kernel(TcsParams p) {
   uint64_t* empty_w = full_w + kTcsWSlots;  // [6]  MMA done with W^T slot
   uint64_t* full_acc = empty_w + kTcsWSlots;  // [8]  accumulator slot t&7 ready
   uint64_t* empty_acc = full_acc + 8;   // [8]  accumulator slot read back
-  float* asum = reinterpret_cast<float*>(empty_acc + 8);  // [16][16][4] per-warp sum_k A[m,k] of tile t&15
-  uint32_t* tslot_ptr = reinterpret_cast<uint32_t*>(asum + 16 * kTcsNB * 4);
+  uint32_t* tslot_ptr = reinterpret_cast<uint32_t*>(empty_acc + 8);
   int* flag = reinterpret_cast<int*>(tslot_ptr + 4);
 
   const int KT = p.K / kBK;
@@ -294,11 +310,10 @@ __global__ void __launch_bounds__(kTcsThreads, 1) tcs_kernel(TcsParams p) {
     };
     // the fixup of tile tp (accumulator slot tp&7), applied one group-iteration late so the
     // dequant never waits for its own MMA
-    auto fixup = [&](int tp, uint16_t scb, uint16_t zb) {
+    // the fixup of tile tp (accumulator slot tp&7): Y += s * c1 * D, applied one group-iteration
+    // late so the dequant never waits for its own MMA
+    auto fixup = [&](int tp, uint16_t scb) {
       const float sc_ = __half2float(__ushort_as_half(scb));
-      float z_ = 0.f;
-      if constexpr (F::kind == kUint) z_ = __half2float(__ushort_as_half(zb));
-      if constexpr (F::kind == kInt) z_ = (float)(1 << (F::bits - 1));
       const int as = tp & 7;
       mbar_wait(&full_acc[as], (tp >> 3) & 1);
       tc_fence_after();
@@ -309,32 +324,34 @@ __global__ void __launch_bounds__(kTcsThreads, 1) tcs_kernel(TcsParams p) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_acc[as]);
       if (lane == 0 && q == 2) tcs_stamp(p, 4, tp);
-      const float c1 = sc_ * c1mul, c2 = -sc_ * z_;
-      const float* as_m = asum + (tp & 15) * kTcsNB * 4;
+      const float c1 = sc_ * c1mul;
 #pragma unroll
-      for (int m = 0; m < MT; ++m) {
-        if (m < p.M) {
-          float v = tot[m];
-          if constexpr (kD2) {
-            const float4 a4 = *reinterpret_cast<const float4*>(as_m + m * 4);  // 4 warps' partial sums
-            v = fmaf(c2, (a4.x + a4.y) + (a4.z + a4.w), v);
-          }
-          tot[m] = fmaf(c1, __uint_as_float(d[m]), v);
-        }
-      }
+      for (int m = 0; m < MT; ++m)
+        if (m < p.M) tot[m] = fmaf(c1, __uint_as_float(d[m]), tot[m]);
       if (lane == 0 && q == 2) tcs_stamp(p, 8, tp);
     };
 
-    uint2 araw_n[RJ];
+    // side inputs (activation slice from L2, scale / zero from HBM) are prefetched two group
+    // iterations ahead into a 2-slot register ring: HBM latency under the weight stream is ~2 us
+    uint2 araw_q[2][RJ];
+    uint16_t sc_q[2] = {0, 0}, z_q[2] = {0, 0};
     int t = g;
     int kk = 0;                  // this group's tile counter (t = g + 3*kk)
-    // (n-tile, k-tile) of this group's current tile and of the next one, tracked incrementally
-    int nt_c = (u0 + t) / KT, kt_c = (u0 + t) - ((u0 + t) / KT) * KT;
-    int nt_n = nt_c, kt_n = kt_c + kTcsGroups;
-    while (kt_n >= KT) { kt_n -= KT; ++nt_n; }
-    if (t < T) load_a(kt_c, araw_n);
+    int nt_f = (u0 + t) / KT, kt_f = (u0 + t) - ((u0 + t) / KT) * KT;  // tile being prefetched
+    auto advance_f = [&]() {
+      kt_f += kTcsGroups;
+      while (kt_f >= KT) { kt_f -= KT; ++nt_f; }
+    };
+#pragma unroll
+    for (int pf = 0; pf < 2; ++pf) {
+      if (t + pf * kTcsGroups < T) {
+        load_a(kt_f, araw_q[pf]);
+        load_sz(nt_f, kt_f, sc_q[pf], z_q[pf]);
+      }
+      advance_f();
+    }
     int tp = -1;                 // this group's tile whose fixup is pending
-    uint16_t sc_p = 0, z_p = 0;  // its scale / zero (fp16 bits)
+    uint16_t sc_p = 0;           // its scale (fp16 bits)
     int t0 = 0;
     while (t0 < T) {
       const int ufirst = u0 + t0;
@@ -345,16 +362,21 @@ __global__ void __launch_bounds__(kTcsThreads, 1) tcs_kernel(TcsParams p) {
         const int ws = 2 * g + (kk & 1);
         const uint32_t tslot = tmem + lane_off + ws * 64;
         const uint32_t ap_u = smem_u32(ap + ws * kTcsApBytes);
+        const int pq = kk & 1;
         uint2 araw[RJ];
 #pragma unroll
-        for (int j = 0; j < RJ; ++j) araw[j] = araw_n[j];
-        if (t + kTcsGroups < T) load_a(kt_n, araw_n);
-        uint16_t sc_c, z_c;
-        load_sz(nt_c, kt_c, sc_c, z_c);  // consumed by this tile's (lagged) fixup
-        nt_c = nt_n;
-        kt_c = kt_n;
-        kt_n += kTcsGroups;
-        while (kt_n >= KT) { kt_n -= KT; ++nt_n; }
+        for (int j = 0; j < RJ; ++j) araw[j] = pq ? araw_q[1][j] : araw_q[0][j];
+        const uint16_t sc_c = pq ? sc_q[1] : sc_q[0], z_c = pq ? z_q[1] : z_q[0];
+        if (t + 2 * kTcsGroups < T) {
+          if (pq) {
+            load_a(kt_f, araw_q[1]);
+            load_sz(nt_f, kt_f, sc_q[1], z_q[1]);
+          } else {
+            load_a(kt_f, araw_q[0]);
+            load_sz(nt_f, kt_f, sc_q[0], z_q[0]);
+          }
+        }
+        advance_f();
         const int s = t & (NS - 1);
         if (lane == 0 && q == 2) tcs_stamp(p, 10, t);
         mbar_wait(&full_tma[s], (t >> p.lg_ns) & 1);
@@ -365,32 +387,23 @@ __global__ void __launch_bounds__(kTcsThreads, 1) tcs_kernel(TcsParams p) {
         tcs_load_words<F::bits>(st_u + s * stage_bytes, n, words);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_tma[s]);   // the stage goes back to the TMA ring now
-        tcs_dequant_tile<F>(words, tslot);
-        // activation operand (prescaled by 2^-P) and the per-warp partial row sums
+        uint32_t cz[11];
+        if constexpr (F::kind == kUint) tcs_zero_consts<F>(__half2float(__ushort_as_half(z_c)), cz);
+        if constexpr (F::kind == kInt) tcs_zero_consts<F>((float)(1 << (F::bits - 1)), cz);
+        tcs_dequant_tile<F>(words, tslot, cz);
+        // activation operand, prescaled by 2^-P per k (ints); this warp converts its k-quarter
 #pragma unroll
         for (int j = 0; j < RJ; ++j) {
           const int m = ar0 + 4 * j;
-          if (j * 4 < p.M) {           // warp-uniform: every lane takes part in the shuffles
-            __half2 a0 = u32_as_h2(0u), a1 = u32_as_h2(0u);
-            if (m < p.M) {
-              a0 = u32_as_h2(araw[j].x);
-              a1 = u32_as_h2(araw[j].y);
-            }
+          if (m < p.M) {
+            __half2 a0 = u32_as_h2(araw[j].x), a1 = u32_as_h2(araw[j].y);
             if constexpr (kD2) {
-              const float2 f0 = __half22float2(a0), f1 = __half22float2(a1);
-              float sum = (f0.x + f0.y) + (f1.x + f1.y);
-              sum += __shfl_xor_sync(0xffffffffu, sum, 4);
-              sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-              sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-              if ((lane & 7) == 0 && m < p.M) asum[((t & 15) * kTcsNB + m) * 4 + q] = sum;
               a0 = __hmul2(a0, pre0h);
               a1 = __hmul2(a1, pre1h);
             }
-            if (m < p.M) {
-              const uint32_t dst = ap_u + a_kb + m * 128 + (((a_c ^ (uint32_t)(m & 7))) << 4) + a_h;
-              asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(dst), "r"(h2_as_u32(a0)), "r"(h2_as_u32(a1))
-                           : "memory");
-            }
+            const uint32_t dst = ap_u + a_kb + m * 128 + (((a_c ^ (uint32_t)(m & 7))) << 4) + a_h;
+            asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(dst), "r"(h2_as_u32(a0)), "r"(h2_as_u32(a1))
+                         : "memory");
           }
         }
         tmem_st_wait();
@@ -399,18 +412,13 @@ __global__ void __launch_bounds__(kTcsThreads, 1) tcs_kernel(TcsParams p) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&full_w[ws]);
         if (lane == 0 && q == 2) tcs_stamp(p, 3, t);
-        if (tp >= 0) {
-          named_bar_sync(2 + g, 128);   // this group's row sums of tile tp are visible
-          fixup(tp, sc_p, z_p);
-        }
+        if (tp >= 0) fixup(tp, sc_p);
         tp = t;
         sc_p = sc_c;
-        z_p = z_c;
       }
       // drain this group's pending fixup before the n-tile is summed
       if (tp >= 0) {
-        named_bar_sync(2 + g, 128);
-        fixup(tp, sc_p, z_p);
+        fixup(tp, sc_p);
         tp = -1;
       }
       // ---- n-tile nt done by this CTA: sum the 4 groups' totals, write Y or a partial ----
