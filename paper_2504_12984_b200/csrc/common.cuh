@@ -230,4 +230,27 @@ __device__ __forceinline__ void load_half_words(const uint8_t* tile, int c, uint
   }
 }
 
+// Raw pair bits for the tensor-core decode path and the CUDA-core GEMV (no magic number):
+//   ints:   the b-bit code u placed at bit P of each 16-bit half IS the fp16 u * 2^(P-24)
+//           (subnormal, or a small normal) -- exact; the activations are pre-scaled by 2^-P
+//   floats: the code's E+M field on the fp16 exponent/mantissa fields and the sign moved to
+//           bit 15: the fp16 value(code) * 2^(bias-15), exact
+template <int B, int I>
+struct SubP {
+  static constexpr int value = PairP<B, I>::value;
+};
+
+template <class F, int I>
+__device__ __forceinline__ uint32_t raw_pair_bits(const uint32_t* words) {
+  if constexpr (F::kind != kFloat) {
+    return assemble_pair<F::bits, I, SubP<F::bits, I>::value>(words);
+  } else {
+    constexpr int P = 10 - F::man;
+    uint32_t x = assemble_pair<F::bits, I, P>(words);
+    constexpr uint32_t sb = 1u << (10 + F::exp);
+    const uint32_t y = x & (sb | (sb << 16));
+    return x + y * ((1u << (5 - F::exp)) - 1u);
+  }
+}
+
 }  // namespace tl

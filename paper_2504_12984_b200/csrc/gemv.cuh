@@ -1,24 +1,28 @@
-// gemv.cu -- decode-shape path (M <= 16) on CUDA cores: SURVEY §8(a) rows a3-a11, K-B2.
+// gemv.cuh -- decode-shape path on CUDA cores: SURVEY §8(a) rows a3-a11, K-B2.
 //
 // Paper: "CUDA Cores for 1-15 tokens"; the weight pipeline of
 // fig:weight-pipeline(c): (1) pipelined asynchronous copy
 // global -> shared, (2) shared -> registers, (3) reinterpret, (4) vectorised cast;
-// plus software pipelining and k-dimension parallelisation (stream-K)
-// (PAPER.md:546).  B200 form:
-//   * a producer warp streams whole 128x128 weight tiles (2048*b contiguous bytes,
-//     one cp.async.bulk each) plus the activation / scale / zero slices of that
-//     k-tile into an NS-stage shared-memory ring guarded by mbarriers;
-//   * 256 consumer threads: thread (c, kh) owns column c of the tile and the k-half
-//     kh; it reads its column's segment words with 16-byte LDS, turns every pair of
-//     codes into an exact fp16x2 (u - z) with one LOP3 + one HFMA2 (common.cuh
-//     pair_value), and accumulates w*A with FHFMA (fp16 x fp16 + fp32 -> fp32, the
-//     PTX fma.rn.f32.f16), i.e. fp32 accumulation (reading R10);
-//     the group scale is applied in fp32 once per (group, k-half) sub-piece;
-//   * stream-K: the linear unit space u = nt*KT + kt (n-tile major = the byte order
-//     of the transformed weight) is cut into `grid` equal contiguous ranges, so
-//     every CTA streams one contiguous byte range and the load is balanced to one
-//     tile; n-tiles shared between CTAs are reduced deterministically (fixed CTA
-//     order) by whichever CTA arrives last (reading R12).
+// plus software pipelining and k-dimension parallelisation (stream-K).
+// B200 form:
+//   * the producer warp streams whole 128x128 weight tiles (2048*b contiguous bytes, one
+//     cp.async.bulk each) and the k-tile's activation rows into an NS-stage shared-memory
+//     ring (mbarriers); a few stages behind, the same warp pre-scales the activations by
+//     2^-P per k and writes the sum of A over every 32-k sub-piece into the stage;
+//   * 256 consumer threads: thread (c, kh) owns column c of the tile and the k-half kh; it
+//     reads its column's segment words with 16-byte LDS; ONE LOP3 per pair of codes places
+//     them in the two fp16 lanes as u * 2^(P-24) (exact fp16 subnormals -- no conversion
+//     instruction at all), and FHFMA (fma.rn.f32.f16: fp16 x fp16 + fp32) accumulates
+//     u * A * 2^-24 exactly in fp32 (reading R10).  The zero point and the
+//     group scale are applied once per 32-k sub-piece: Y += s * (2^24 * acc - z * sum(A));
+//     float codes are placed on the fp16 exponent/mantissa fields (value * 2^(bias-15)) and
+//     Y += s * 2^(15-bias) * acc;
+//   * scales and zero points are read by the consumers straight from global memory, two tiles
+//     ahead, so the TMA ring carries only two bulk copies per tile;
+//   * stream-K: the linear unit space u = nt*KT + kt (n-tile major = the byte order of the
+//     transformed weight) is cut into `grid` equal contiguous ranges, so every CTA streams one
+//     contiguous byte range; n-tiles shared between CTAs are reduced deterministically (fixed
+//     CTA order) by whichever CTA arrives last (reading R12).
 #pragma once
 #include "paths.cuh"
 #include "ptx.cuh"
@@ -31,12 +35,13 @@ constexpr int kGemvThreads = kGemvConsumers + 32;
 template <class F, int MT>
 struct GemvLayout {
   static constexpr int w_bytes = tile_bytes(F::bits);
-  static constexpr int a_bytes = MT * kBK * 2;  // fp16 [MT][128]
-  static constexpr int sz_bytes = 4 * kBN * 2;  // up to 4 group rows of 128 fp16
-  static constexpr int stage_bytes = w_bytes + a_bytes + 2 * sz_bytes;
-  static constexpr int stages = (stage_bytes * 8 <= 96 * 1024) ? 8 : ((stage_bytes * 4 <= 96 * 1024) ? 4 : 3);
+  static constexpr int a_bytes = MT * kBK * 2;      // activations A'[MT][128] fp16 (pre-scaled in place)
+  static constexpr int s_bytes = MT * 4 * 4;        // sum_k A over each 32-k sub-piece, fp32 [MT][4]
+  static constexpr int stage_bytes = (w_bytes + a_bytes + s_bytes + 127) / 128 * 128;
+  static constexpr int stages_raw = (96 * 1024) / stage_bytes;
+  static constexpr int stages = stages_raw < 4 ? 4 : (stages_raw > 16 ? 16 : stages_raw);
   static constexpr int red_bytes = MT * kBN * 4;
-  static constexpr int smem = stages * stage_bytes + red_bytes + 2 * stages * 8 + 16;
+  static constexpr int smem = stages * stage_bytes + red_bytes + 3 * stages * 8 + 16;
 };
 
 __device__ __forceinline__ float fhfma(uint16_t a, uint16_t b, float c) {
@@ -44,57 +49,24 @@ __device__ __forceinline__ float fhfma(uint16_t a, uint16_t b, float c) {
   return c;
 }
 
+// One k-half of one tile for column c.  sc/zc: fp16 bits of the scale / zero of the half's
+// two 32-k sub-pieces.
 template <class F, int MT, int KH>
-__device__ __forceinline__ void gemv_tile_half(const uint8_t* stage, int c, uint32_t magic, int G, bool has_zeros,
-                                               float (&tot)[MT]) {
+__device__ __forceinline__ void gemv_tile_half(const uint8_t* stage, int c, const uint16_t (&sc)[2],
+                                               const uint16_t (&zc)[2], float (&tot)[MT]) {
   using L = GemvLayout<F, MT>;
   constexpr int B = F::bits;
-  // this thread's words: segment s, words j in [2w*KH, 2w*KH + 2w)
   uint32_t words[4 * B];
-#pragma unroll
-  for (int s = 0; s < F::nseg; ++s) {
-    constexpr int dummy = 0;
-    (void)dummy;
-    const int w = seg_width(B, s), base = seg_base(B, s);
-    const uint8_t* sp = stage + 2048 * base;
-    if (w == 1) {
-      const uint2 x = *reinterpret_cast<const uint2*>(sp + c * 16 + KH * 8);
-      words[4 * base + 2 * KH + 0] = x.x;
-      words[4 * base + 2 * KH + 1] = x.y;
-    } else {
-#pragma unroll
-      for (int v = 0; v < w / 2; ++v) {
-        const int vv = KH * (w / 2) + v;
-        const uint4 x = *reinterpret_cast<const uint4*>(sp + (vv * 128 + c) * 16);
-        words[4 * base + 4 * vv + 0] = x.x;
-        words[4 * base + 4 * vv + 1] = x.y;
-        words[4 * base + 4 * vv + 2] = x.z;
-        words[4 * base + 4 * vv + 3] = x.w;
-      }
-    }
-  }
+  load_half_words<B, KH>(stage, c, words);
   const __half* As = reinterpret_cast<const __half*>(stage + L::w_bytes);
-  const __half* Ss = reinterpret_cast<const __half*>(stage + L::w_bytes + L::a_bytes);
-  const __half* Zs = reinterpret_cast<const __half*>(stage + L::w_bytes + L::a_bytes + L::sz_bytes);
-  // sub-pieces of 32 k (16 pairs): every group boundary (G = 32, 64, 128*j) is one
-  const int lg = G == 32 ? 5 : 6;          // log2 G for G < 128
+  const float* Ss = reinterpret_cast<const float*>(stage + L::w_bytes + L::a_bytes);
   float acc[MT];
 #pragma unroll
   for (int m = 0; m < MT; ++m) acc[m] = 0.f;
-  PairConsts pc;
-  pc.magic = magic;
-  float s = 0.f;
   static_for<0, 32>([&](auto II) {
-    constexpr int i = KH * 32 + decltype(II)::value;
-    if constexpr (i % 16 == 0) {
-      const int r = (G >= kBK) ? 0 : ((2 * i) >> lg);  // group row of this sub-piece in the stage slice
-      s = __half2float(Ss[r * kBN + c]);
-      float z = 0.f;
-      if constexpr (F::kind == kUint) z = has_zeros ? __half2float(Zs[r * kBN + c]) : 0.f;
-      if constexpr (F::kind == kInt) z = (float)(1 << (B - 1));
-      make_pair_consts<F>(pc, z);
-    }
-    const uint32_t wp = h2_as_u32(pair_value<F, i>(words, pc));
+    constexpr int ii = decltype(II)::value;
+    constexpr int i = KH * 32 + ii;
+    const uint32_t wp = raw_pair_bits<F, i>(words);
     const uint16_t wlo = (uint16_t)(wp & 0xFFFF), whi = (uint16_t)(wp >> 16);
 #pragma unroll
     for (int m = 0; m < MT; ++m) {
@@ -102,11 +74,27 @@ __device__ __forceinline__ void gemv_tile_half(const uint8_t* stage, int c, uint
       acc[m] = fhfma(wlo, (uint16_t)(a2 & 0xFFFF), acc[m]);
       acc[m] = fhfma(whi, (uint16_t)(a2 >> 16), acc[m]);
     }
-    if constexpr (i % 16 == 15) {
+    if constexpr (ii % 16 == 15) {
+      constexpr int h = ii / 16;               // sub-piece within the half
+      constexpr int sp = KH * 2 + h;           // sub-piece within the tile
+      const float s = __half2float(__ushort_as_half(sc[h]));
+      if constexpr (F::kind != kFloat) {
+        float z = 0.f;
+        if constexpr (F::kind == kUint) z = __half2float(__ushort_as_half(zc[h]));
+        if constexpr (F::kind == kInt) z = (float)(1 << (B - 1));
+        const float c1 = s * 16777216.f, c2 = -s * z;
 #pragma unroll
-      for (int m = 0; m < MT; ++m) {
-        tot[m] = fmaf(s, acc[m], tot[m]);
-        acc[m] = 0.f;
+        for (int m = 0; m < MT; ++m) {
+          tot[m] = fmaf(c2, Ss[m * 4 + sp], fmaf(c1, acc[m], tot[m]));
+          acc[m] = 0.f;
+        }
+      } else {
+        const float c1 = s * (float)(1 << (15 - F::bias));
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+          tot[m] = fmaf(c1, acc[m], tot[m]);
+          acc[m] = 0.f;
+        }
       }
     }
   });
@@ -116,10 +104,12 @@ template <class F, int MT>
 __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvParams p) {
   using L = GemvLayout<F, MT>;
   constexpr int NS = L::stages;
+  constexpr bool kPre = F::kind != kFloat;  // integer codes: pre-scale A by 2^-P, need sum(A)
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* stages = smem;
   float* red = reinterpret_cast<float*>(smem + NS * L::stage_bytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * L::stage_bytes + L::red_bytes);
+  uint64_t* full_tma = reinterpret_cast<uint64_t*>(smem + NS * L::stage_bytes + L::red_bytes);
+  uint64_t* full = full_tma + NS;   // stage prepared (activations pre-scaled, sums written)
   uint64_t* empty = full + NS;
   int* flag = reinterpret_cast<int*>(empty + NS);
 
@@ -128,52 +118,76 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvParams p) {
   const int cta = blockIdx.x;
   const int u0 = (int)((int64_t)cta * p.units / grid);
   const int u1 = (int)((int64_t)(cta + 1) * p.units / grid);
+  const int T = u1 - u0;
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
+  const int lane = tid & 31;
 
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
+      mbar_init(&full_tma[s], 1);
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kGemvConsumers / 32);
     }
     fence_mbar_init();
   }
-  // zero the activation rows >= M of every stage once (TMA never writes them)
-  for (int s = 0; s < NS; ++s) {
-    __half* As = reinterpret_cast<__half*>(stages + s * L::stage_bytes + L::w_bytes);
-    for (int e = tid; e < (MT - p.M) * kBK; e += kGemvThreads) As[p.M * kBK + e] = __float2half_rn(0.f);
-  }
-  fence_proxy_async_smem();
   __syncthreads();
-
-  const int spt = p.G >= kBK ? 1 : kBK / p.G;  // group rows per tile
-  const bool has_zeros = p.zeros != nullptr;
 
   if (warp == kGemvConsumers / 32) {
     // ---------------- producer warp ----------------
-    if (elect_one()) {
-      const uint64_t pol_w = policy_evict_first();
-      const uint64_t pol_a = policy_evict_last();
-      const uint32_t bytes = L::w_bytes + p.M * kBK * 2 + spt * kBN * 2 * (has_zeros ? 2 : 1);
-      int s = 0, ph = 0, nt = u0 / KT, kt = u0 % KT;
-      for (int u = u0; u < u1; ++u) {
-        if (u - u0 >= NS) mbar_wait(&empty[s], ph ^ 1);
+    const uint64_t pol_w = policy_evict_first();
+    const uint64_t pol_a = policy_evict_last();
+    const uint32_t bytes = L::w_bytes + p.M * kBK * 2;
+    constexpr int D = NS - 2;  // how far the bulk copies run ahead of the preparation
+    auto issue = [&](int t) {
+      const int s = t % NS;
+      if (t >= NS) mbar_wait(&empty[s], ((t / NS) - 1) & 1);
+      if (lane == 0) {
+        const int u = u0 + t, kt = u % KT;
         uint8_t* st = stages + s * L::stage_bytes;
-        mbar_arrive_expect_tx(&full[s], bytes);
-        tma_bulk_g2s(st, p.wt + (int64_t)u * L::w_bytes, L::w_bytes, &full[s], pol_w);
+        mbar_arrive_expect_tx(&full_tma[s], bytes);
+        tma_bulk_g2s(st, p.wt + (int64_t)u * L::w_bytes, L::w_bytes, &full_tma[s], pol_w);
         for (int m = 0; m < p.M; ++m)
-          tma_bulk_g2s(st + L::w_bytes + m * kBK * 2, p.A + m * p.lda + (int64_t)kt * kBK, kBK * 2, &full[s], pol_a);
-        const int g0 = (int)((int64_t)kt * kBK / p.G);
-        for (int r = 0; r < spt; ++r) {
-          tma_bulk_g2s(st + L::w_bytes + L::a_bytes + r * kBN * 2, p.scales + (int64_t)(g0 + r) * p.N + nt * kBN,
-                       kBN * 2, &full[s], pol_w);
-          if (has_zeros)
-            tma_bulk_g2s(st + L::w_bytes + L::a_bytes + L::sz_bytes + r * kBN * 2,
-                         p.zeros + (int64_t)(g0 + r) * p.N + nt * kBN, kBN * 2, &full[s], pol_w);
-        }
-        if (++kt == KT) { kt = 0; ++nt; }
-        if (++s == NS) { s = 0; ph ^= 1; }
+          tma_bulk_g2s(st + L::w_bytes + m * kBK * 2, p.A + m * p.lda + (int64_t)kt * kBK, kBK * 2, &full_tma[s],
+                       pol_a);
       }
+      __syncwarp();
+    };
+    // per-lane pre-scale factors: lane L owns k = 4L..4L+3 = pairs 2L, 2L+1
+    __half2 pre0 = __float2half2_rn(1.f), pre1 = __float2half2_rn(1.f);
+    if constexpr (kPre) {
+      int P0 = 0, P1 = 0;
+      static_for<0, 64>([&](auto II) {
+        constexpr int i = decltype(II)::value;
+        if (i == 2 * lane) P0 = SubP<F::bits, i>::value;
+        if (i == 2 * lane + 1) P1 = SubP<F::bits, i>::value;
+      });
+      pre0 = __float2half2_rn(__int_as_float((127 - P0) << 23));
+      pre1 = __float2half2_rn(__int_as_float((127 - P1) << 23));
+    }
+    for (int t = 0; t < D && t < T; ++t) issue(t);
+    for (int t = 0; t < T; ++t) {
+      if (t + D < T) issue(t + D);
+      const int s = t % NS;
+      mbar_wait(&full_tma[s], (t / NS) & 1);
+      if constexpr (kPre) {
+        uint8_t* st = stages + s * L::stage_bytes;
+        for (int m = 0; m < p.M; ++m) {
+          uint2* ap = reinterpret_cast<uint2*>(st + L::w_bytes + m * kBK * 2) + lane;
+          const uint2 a = *ap;
+          const float2 f0 = __half22float2(u32_as_h2(a.x)), f1 = __half22float2(u32_as_h2(a.y));
+          float sum = (f0.x + f0.y) + (f1.x + f1.y);
+          sum += __shfl_xor_sync(0xffffffffu, sum, 4);
+          sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+          sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+          if ((lane & 7) == 0)
+            reinterpret_cast<float*>(st + L::w_bytes + L::a_bytes)[m * 4 + (lane >> 3)] = sum;
+          *ap = make_uint2(h2_as_u32(__hmul2(u32_as_h2(a.x), pre0)), h2_as_u32(__hmul2(u32_as_h2(a.y), pre1)));
+        }
+      }
+      fence_proxy_async_smem();  // order these generic writes before the stage's next TMA refill
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[s]);
     }
     return;
   }
@@ -184,15 +198,48 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvParams p) {
   float tot[MT];
 #pragma unroll
   for (int m = 0; m < MT; ++m) tot[m] = 0.f;
+  const bool has_zeros = p.zeros != nullptr;
+  const unsigned short* sg = reinterpret_cast<const unsigned short*>(p.scales);
+  const unsigned short* zg = reinterpret_cast<const unsigned short*>(p.zeros);
+  // scale / zero rows of this thread's two sub-pieces of tile (nt, kt)
+  auto load_sz = [&](int nt, int kt, uint16_t (&sc)[2], uint16_t (&zc)[2]) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k = kt * kBK + kh * 64 + h * 32;
+      const int64_t off = (int64_t)(k / p.G) * p.N + nt * kBN + c;
+      sc[h] = __ldg(sg + off);
+      zc[h] = (F::kind == kUint && has_zeros) ? __ldg(zg + off) : (unsigned short)0;
+    }
+  };
+  uint16_t scq[2][2], zcq[2][2];  // two-tile-deep prefetch ring
+  int nt_f = u0 / KT, kt_f = u0 % KT;
+#pragma unroll
+  for (int pf = 0; pf < 2; ++pf) {
+    if (pf < T) load_sz(nt_f, kt_f, scq[pf], zcq[pf]);
+    if (++kt_f == KT) { kt_f = 0; ++nt_f; }
+  }
 
   int s = 0, ph = 0, nt = u0 / KT, kt = u0 % KT;
   for (int u = u0; u < u1; ++u) {
+    const int t = u - u0;
+    const int pq = t & 1;
+    uint16_t sc[2], zc[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      sc[h] = pq ? scq[1][h] : scq[0][h];
+      zc[h] = pq ? zcq[1][h] : zcq[0][h];
+    }
+    if (t + 2 < T) {
+      if (pq) load_sz(nt_f, kt_f, scq[1], zcq[1]);
+      else load_sz(nt_f, kt_f, scq[0], zcq[0]);
+      if (++kt_f == KT) { kt_f = 0; ++nt_f; }
+    }
     mbar_wait(&full[s], ph);
     const uint8_t* st = stages + s * L::stage_bytes;
-    if (kh == 0) gemv_tile_half<F, MT, 0>(st, c, p.magic, p.G, has_zeros, tot);
-    else gemv_tile_half<F, MT, 1>(st, c, p.magic, p.G, has_zeros, tot);
+    if (kh == 0) gemv_tile_half<F, MT, 0>(st, c, sc, zc, tot);
+    else gemv_tile_half<F, MT, 1>(st, c, sc, zc, tot);
     __syncwarp();
-    if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+    if (lane == 0) mbar_arrive(&empty[s]);
     if (++s == NS) { s = 0; ph ^= 1; }
     const int cur_nt = nt, cur_kt = kt;
     if (++kt == KT) { kt = 0; ++nt; }

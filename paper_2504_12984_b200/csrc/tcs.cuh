@@ -58,11 +58,6 @@ constexpr int kTcsWSlots = 2 * kTcsGroups;        // W^T tiles in TMEM (64 colum
 // TMEM columns: W^T slots [0,384) (6 x 64), accumulators [384,512) (8 x 16)
 constexpr uint32_t kTcsAccCol = 64 * kTcsWSlots;
 
-template <int B, int I>
-struct SubP {  // bit position of pair I's code in each 16-bit half (same rule as PairP)
-  static constexpr int value = PairP<B, I>::value;
-};
-
 __device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
@@ -93,20 +88,6 @@ __device__ __forceinline__ uint64_t sw128_desc_s(uint32_t saddr) {
   return d;
 }
 
-// fp16 bits of the raw pair (no magic): ints -> subnormal u*2^(P-24); floats -> value*2^(bias-15)
-template <class F, int I>
-__device__ __forceinline__ uint32_t tcs_pair_bits(const uint32_t* words) {
-  if constexpr (F::kind != kFloat) {
-    return assemble_pair<F::bits, I, SubP<F::bits, I>::value>(words);
-  } else {
-    constexpr int P = 10 - F::man;
-    uint32_t x = assemble_pair<F::bits, I, P>(words);
-    constexpr uint32_t sb = 1u << (10 + F::exp);
-    const uint32_t y = x & (sb | (sb << 16));
-    return x + y * ((1u << (5 - F::exp)) - 1u);
-  }
-}
-
 template <int B>
 __device__ __forceinline__ void tcs_load_words(uint32_t wtile, int n, uint32_t* words) {
 #pragma unroll
@@ -135,7 +116,7 @@ __device__ __forceinline__ void tcs_dequant_tile(const uint32_t* words, uint32_t
     static_for<0, 16>([&](auto II) {
       constexpr int ii = decltype(II)::value;
       constexpr int i = c * 16 + ii;
-      const uint32_t x = tcs_pair_bits<F, i>(words);
+      const uint32_t x = raw_pair_bits<F, i>(words);
       if constexpr (F::kind != kFloat) r[ii] = h2_as_u32(__hsub2(u32_as_h2(x), u32_as_h2(cz[SubP<F::bits, i>::value])));
       else r[ii] = x;
     });
