@@ -16,7 +16,7 @@ import re
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtilus_b200.so")
+LIB_PATH = os.environ.get("TL_LIB_PATH") or os.path.join(_HERE, "libtilus_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

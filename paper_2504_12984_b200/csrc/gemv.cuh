@@ -30,7 +30,7 @@
 namespace tl {
 
 constexpr int kGemvConsumers = 256;
-constexpr int kGemvThreads = kGemvConsumers + 32;
+constexpr int kGemvThreads = kGemvConsumers + 64;  // + TMA issuer warp + preparation warp
 
 template <class F, int MT>
 struct GemvLayout {
@@ -44,8 +44,15 @@ struct GemvLayout {
   static constexpr int smem = stages * stage_bytes + red_bytes + 3 * stages * 8 + 16;
 };
 
-__device__ __forceinline__ float fhfma(uint16_t a, uint16_t b, float c) {
-  asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(c) : "h"(a), "h"(b));
+// acc += w.lo * a.lo + w.hi * a.hi  (two FHFMA reading the 16-bit halves in place)
+__device__ __forceinline__ float fhfma2(uint32_t w, uint32_t a, float c) {
+  asm("{\n\t.reg .b16 wl, wh, al, ah;\n\t"
+      "mov.b32 {wl, wh}, %1;\n\t"
+      "mov.b32 {al, ah}, %2;\n\t"
+      "fma.rn.f32.f16 %0, wl, al, %0;\n\t"
+      "fma.rn.f32.f16 %0, wh, ah, %0;\n\t}"
+      : "+f"(c)
+      : "r"(w), "r"(a));
   return c;
 }
 
@@ -67,13 +74,9 @@ __device__ __forceinline__ void gemv_tile_half(const uint8_t* stage, int c, cons
     constexpr int ii = decltype(II)::value;
     constexpr int i = KH * 32 + ii;
     const uint32_t wp = raw_pair_bits<F, i>(words);
-    const uint16_t wlo = (uint16_t)(wp & 0xFFFF), whi = (uint16_t)(wp >> 16);
 #pragma unroll
-    for (int m = 0; m < MT; ++m) {
-      const uint32_t a2 = *reinterpret_cast<const uint32_t*>(As + m * kBK + 2 * i);
-      acc[m] = fhfma(wlo, (uint16_t)(a2 & 0xFFFF), acc[m]);
-      acc[m] = fhfma(whi, (uint16_t)(a2 >> 16), acc[m]);
-    }
+    for (int m = 0; m < MT; ++m)
+      acc[m] = fhfma2(wp, *reinterpret_cast<const uint32_t*>(As + m * kBK + 2 * i), acc[m]);
     if constexpr (ii % 16 == 15) {
       constexpr int h = ii / 16;               // sub-piece within the half
       constexpr int sp = KH * 2 + h;           // sub-piece within the tile
@@ -134,26 +137,29 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvParams p) {
   __syncthreads();
 
   if (warp == kGemvConsumers / 32) {
-    // ---------------- producer warp ----------------
-    const uint64_t pol_w = policy_evict_first();
-    const uint64_t pol_a = policy_evict_last();
-    const uint32_t bytes = L::w_bytes + p.M * kBK * 2;
-    constexpr int D = NS - 2;  // how far the bulk copies run ahead of the preparation
-    auto issue = [&](int t) {
-      const int s = t % NS;
-      if (t >= NS) mbar_wait(&empty[s], ((t / NS) - 1) & 1);
-      if (lane == 0) {
-        const int u = u0 + t, kt = u % KT;
+    // ---------------- TMA issuer warp: weight tile + activation rows per stage ----------------
+    if (elect_one()) {
+      const uint64_t pol_w = policy_evict_first();
+      const uint64_t pol_a = policy_evict_last();
+      const uint32_t bytes = L::w_bytes + p.M * kBK * 2;
+      int s = 0, ph = 0, kt = u0 % KT;
+      for (int t = 0; t < T; ++t) {
+        if (t >= NS) mbar_wait_sleepy(&empty[s], ph ^ 1);
         uint8_t* st = stages + s * L::stage_bytes;
         mbar_arrive_expect_tx(&full_tma[s], bytes);
-        tma_bulk_g2s(st, p.wt + (int64_t)u * L::w_bytes, L::w_bytes, &full_tma[s], pol_w);
+        tma_bulk_g2s(st, p.wt + (int64_t)(u0 + t) * L::w_bytes, L::w_bytes, &full_tma[s], pol_w);
         for (int m = 0; m < p.M; ++m)
           tma_bulk_g2s(st + L::w_bytes + m * kBK * 2, p.A + m * p.lda + (int64_t)kt * kBK, kBK * 2, &full_tma[s],
                        pol_a);
+        if (++kt == KT) kt = 0;
+        if (++s == NS) { s = 0; ph ^= 1; }
       }
-      __syncwarp();
-    };
-    // per-lane pre-scale factors: lane L owns k = 4L..4L+3 = pairs 2L, 2L+1
+    }
+    return;
+  }
+  if (warp == kGemvConsumers / 32 + 1) {
+    // ---------------- preparation warp: pre-scale the activations, sub-piece sums ----------------
+    // lane L owns k = 4L..4L+3 = pairs 2L, 2L+1
     __half2 pre0 = __float2half2_rn(1.f), pre1 = __float2half2_rn(1.f);
     if constexpr (kPre) {
       int P0 = 0, P1 = 0;
@@ -165,11 +171,9 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvParams p) {
       pre0 = __float2half2_rn(__int_as_float((127 - P0) << 23));
       pre1 = __float2half2_rn(__int_as_float((127 - P1) << 23));
     }
-    for (int t = 0; t < D && t < T; ++t) issue(t);
+    int s = 0, ph = 0;
     for (int t = 0; t < T; ++t) {
-      if (t + D < T) issue(t + D);
-      const int s = t % NS;
-      mbar_wait(&full_tma[s], (t / NS) & 1);
+      mbar_wait(&full_tma[s], ph);
       if constexpr (kPre) {
         uint8_t* st = stages + s * L::stage_bytes;
         for (int m = 0; m < p.M; ++m) {
@@ -184,10 +188,11 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvParams p) {
             reinterpret_cast<float*>(st + L::w_bytes + L::a_bytes)[m * 4 + (lane >> 3)] = sum;
           *ap = make_uint2(h2_as_u32(__hmul2(u32_as_h2(a.x), pre0)), h2_as_u32(__hmul2(u32_as_h2(a.y), pre1)));
         }
+        fence_proxy_async_smem();  // order these generic writes before the stage's next TMA refill
       }
-      fence_proxy_async_smem();  // order these generic writes before the stage's next TMA refill
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[s]);
+      if (++s == NS) { s = 0; ph ^= 1; }
     }
     return;
   }
@@ -202,38 +207,48 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvParams p) {
   const unsigned short* sg = reinterpret_cast<const unsigned short*>(p.scales);
   const unsigned short* zg = reinterpret_cast<const unsigned short*>(p.zeros);
   // scale / zero rows of this thread's two sub-pieces of tile (nt, kt)
-  auto load_sz = [&](int nt, int kt, uint16_t (&sc)[2], uint16_t (&zc)[2]) {
+  // Scale / zero prefetch, PF tiles ahead (HBM latency under the weight stream is ~2 us): a
+  // shift register of fp16 bits.  The group row of the prefetched tile is tracked incrementally.
+  constexpr int PF = 4;
+  const int lgG = p.G == 32 ? 5 : (p.G == 64 ? 6 : 0);   // G < 128: row = (k >> lgG)
+  const int tpg = p.G >= kBK ? p.G / kBK : 1;             // G >= 128: k-tiles per group
+  int nt_f = u0 / KT, kt_f = u0 % KT;
+  int grow = lgG ? 0 : kt_f / tpg, grem = lgG ? 0 : kt_f % tpg;
+  auto fetch = [&](uint16_t (&sc)[2], uint16_t (&zc)[2]) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int k = kt * kBK + kh * 64 + h * 32;
-      const int64_t off = (int64_t)(k / p.G) * p.N + nt * kBN + c;
+      const int row = lgG ? ((kt_f * kBK + kh * 64 + h * 32) >> lgG) : grow;
+      const int64_t off = (int64_t)row * p.N + nt_f * kBN + c;
       sc[h] = __ldg(sg + off);
       zc[h] = (F::kind == kUint && has_zeros) ? __ldg(zg + off) : (unsigned short)0;
     }
+    if (++kt_f == KT) {
+      kt_f = 0;
+      ++nt_f;
+      grow = 0;
+      grem = 0;
+    } else if (++grem == tpg) {
+      grem = 0;
+      ++grow;
+    }
   };
-  uint16_t scq[2][2], zcq[2][2];  // two-tile-deep prefetch ring
-  int nt_f = u0 / KT, kt_f = u0 % KT;
+  uint16_t scq[PF][2], zcq[PF][2];
 #pragma unroll
-  for (int pf = 0; pf < 2; ++pf) {
-    if (pf < T) load_sz(nt_f, kt_f, scq[pf], zcq[pf]);
-    if (++kt_f == KT) { kt_f = 0; ++nt_f; }
-  }
+  for (int pf = 0; pf < PF; ++pf)
+    if (pf < T) fetch(scq[pf], zcq[pf]);
 
   int s = 0, ph = 0, nt = u0 / KT, kt = u0 % KT;
   for (int u = u0; u < u1; ++u) {
     const int t = u - u0;
-    const int pq = t & 1;
-    uint16_t sc[2], zc[2];
+    uint16_t sc[2] = {scq[0][0], scq[0][1]}, zc[2] = {zcq[0][0], zcq[0][1]};
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      sc[h] = pq ? scq[1][h] : scq[0][h];
-      zc[h] = pq ? zcq[1][h] : zcq[0][h];
+    for (int pf = 0; pf + 1 < PF; ++pf) {
+      scq[pf][0] = scq[pf + 1][0];
+      scq[pf][1] = scq[pf + 1][1];
+      zcq[pf][0] = zcq[pf + 1][0];
+      zcq[pf][1] = zcq[pf + 1][1];
     }
-    if (t + 2 < T) {
-      if (pq) load_sz(nt_f, kt_f, scq[1], zcq[1]);
-      else load_sz(nt_f, kt_f, scq[0], zcq[0]);
-      if (++kt_f == KT) { kt_f = 0; ++nt_f; }
-    }
+    if (t + PF < T) fetch(scq[PF - 1], zcq[PF - 1]);
     mbar_wait(&full[s], ph);
     const uint8_t* st = stages + s * L::stage_bytes;
     if (kh == 0) gemv_tile_half<F, MT, 0>(st, c, sc, zc, tot);
