@@ -6,13 +6,13 @@
 #include <cstdlib>
 #include <mutex>
 
-#include "tc.cuh"
+#include "tc2.cuh"
 #include "tcs.cuh"
 
 namespace tl {
 
 template <class F>
-tl_status launch_tc(const TcParams& p, const CUtensorMap* tmap, int grid, uint32_t smem_bytes, cudaStream_t st);
+tl_status launch_tc2(const Tc2Params& p, const CUtensorMap* tmap, int grid, uint32_t smem_bytes, cudaStream_t st);
 
 template <class F>
 tl_status launch_tcs(const TcsParams& p, int grid, uint32_t smem_bytes, cudaStream_t st);
@@ -91,7 +91,7 @@ static int round_up(int x, int m) { return (x + m - 1) / m * m; }
 size_t tc_workspace_bytes(int64_t M, int64_t N, int64_t K) {
   (void)N;
   (void)K;
-  const int nb = round_up((int)(M < 256 ? M : 256), 16);
+  const int nb = round_up((int)(M < 128 ? M : 128), 16);
   return (size_t)kTcMaxCtas * 2 * nb * 128 * 4;
 }
 
@@ -131,9 +131,9 @@ tl_status tc_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, cons
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (sms > kTcMaxCtas) sms = kTcMaxCtas;
-  for (int64_t m0 = 0; m0 < M; m0 += 256) {
-    const int mc = (int)((M - m0) < 256 ? (M - m0) : 256);
-    TcParams p{};
+  for (int64_t m0 = 0; m0 < M; m0 += 128) {
+    const int mc = (int)((M - m0) < 128 ? (M - m0) : 128);
+    Tc2Params p{};
     p.M = mc;
     p.N = (int)N;
     p.K = (int)K;
@@ -148,26 +148,18 @@ tl_status tc_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, cons
     p.partial = partial;
     p.sem = sem;
     p.magic = 0x64006400u;
-    int cols = 32;
-    while (cols < 2 * p.NB) cols <<= 1;
-    p.tmem_cols = (uint32_t)cols;
-    // shared memory: 2 x 32 KB dequant tiles, then NS x (activation boxes, packed tile, scale/zero slice)
+    // stage: [activation boxes NB x 256 B (1024-aligned, 128B swizzle) | packed weight tile]
     const uint32_t wb = (uint32_t)tile_bytes(w.bits);
-    const uint32_t astage = (uint32_t)p.NB * 256;
-    const uint32_t budget = 227 * 1024 - 1024 - 256;
-    auto need = [&](int ns, int nd) { return (uint32_t)nd * kDeqBytes + (uint32_t)ns * (astage + wb + 2048); };
-    int ns = 8, nd = 4;
-    while (ns > 3 && need(ns, nd) > budget) --ns;
-    while (nd > 2 && need(ns, nd) > budget) --nd;
-    while (ns > 2 && need(ns, nd) > budget) --ns;
+    p.a_off_in_stage = (uint32_t)p.NB * 256;
+    p.stage_bytes = (p.a_off_in_stage + wb + 1023) & ~1023u;
+    const uint32_t budget = 227 * 1024 - 1024 - 512;
+    int ns = 16;
+    while (ns > 2 && (uint32_t)ns * p.stage_bytes > budget) --ns;
     p.ns = ns;
-    p.nd = nd;
-    p.a_off = nd * kDeqBytes;
-    p.w_off = p.a_off + ns * astage;
-    p.sz_off = p.w_off + ns * wb;
-    p.bar_off = (p.sz_off + ns * 2048 + 7) & ~7u;
-    const uint32_t smem = p.bar_off + (2 * ns + 12) * 8 + 32 + 1024;
-    if (smem > 227 * 1024) return fail(TL_EUNSUPPORTED, "tensor-core tile does not fit shared memory");
+    const uint32_t smem = ns * p.stage_bytes + (2 * ns + 2 * kTc2WSlots + 2) * 8 + 32 + 1024;
+    if (smem > 227 * 1024)
+      return fail(TL_EUNSUPPORTED, "tensor-core tile does not fit shared memory (ns=%d stage=%u smem=%u)", ns,
+                  p.stage_bytes, smem);
     CUtensorMap tmap;
     tl_status s = make_tmap_a(&tmap, A + m0 * lda, mc, K, lda, p.NB);
     if (s != TL_OK) return s;
@@ -177,7 +169,7 @@ tl_status tc_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, cons
     s = TL_EUNSUPPORTED;
     dispatch_format(w.kind, w.bits, w.kind == 2 ? w.exp_bits : 0, [&](auto f) {
       using F = decltype(f);
-      s = launch_tc<F>(p, &tmap, grid, smem, st);
+      s = launch_tc2<F>(p, &tmap, grid, smem, st);
     });
     if (s != TL_OK) return s;
   }
