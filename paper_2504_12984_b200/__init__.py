@@ -6,7 +6,7 @@ unsigned formats, zero points.  The product is the C-ABI library
 ``libtilus_b200.so`` (include/tilus_b200.h); this package is its thin ctypes
 binding (``_lib``) plus the N-sharded multi-GPU wrapper (``dist``).
 
-The library must be built (``python -m paper_2504_12984_b200.build``); there is
+The library must be built (``python paper_2504_12984_b200/build.py``); there is
 no CPU fallback.
 """
 

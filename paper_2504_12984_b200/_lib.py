@@ -20,7 +20,7 @@ LIB_PATH = os.environ.get("TL_LIB_PATH") or os.path.join(_HERE, "libtilus_b200.s
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
-        f"{LIB_PATH} not found: build it with `python -m paper_2504_12984_b200.build` "
+        f"{LIB_PATH} not found: build it with `python paper_2504_12984_b200/build.py` "
         "(there is no CPU fallback for the A16Wx matmul)")
 
 _lib = ctypes.CDLL(LIB_PATH)
