@@ -7,6 +7,7 @@
 #include <mutex>
 
 #include "tc2.cuh"
+#include "tcd.cuh"
 #include "tcs.cuh"
 
 namespace tl {
@@ -17,11 +18,84 @@ tl_status launch_tc2(const Tc2Params& p, const CUtensorMap* tmap, int grid, uint
 template <class F>
 tl_status launch_tcs(const TcsParams& p, int grid, uint32_t smem_bytes, cudaStream_t st);
 
+template <class F>
+tl_status launch_tcd(const TcdParams& p, const CUtensorMap* tmap, int grid, uint32_t smem_bytes, cudaStream_t st);
+
+static tl_status make_tmap_a(CUtensorMap* m, const __half* A, int64_t M, int64_t K, int64_t lda, int NB);
+
 long long* g_trace = nullptr;  // debug: clock64 stamps of CTA 0 (TL_TRACE=1)
 
 bool tc_available() { return true; }
 
 bool tcs_eligible(int64_t M, int32_t G) { return M >= 1 && M <= kTcsNB && G >= kBK; }
+
+static int env_dbg(const char* name) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : 0;
+}
+
+// decode tensor-core path, v2 (tcd.cuh): every side input rides in the TMA stage
+static tl_status tcd_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, const __half* A, int64_t lda,
+                            const uint8_t* wt, const __half* scales, const __half* zeros, __half* Y, int64_t ldy,
+                            float* partial, int* sem, int grid_req, cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (sms > 160) sms = 160;
+  TcdParams p{};
+  p.M = (int)M;
+  p.N = (int)N;
+  p.K = (int)K;
+  p.G = G;
+  p.units = (int)((N / kBN) * (K / kBK));
+  p.wt = wt;
+  p.A = A;
+  p.lda = lda;
+  p.scales = scales;
+  p.zeros = zeros;
+  p.Y = Y;
+  p.ldy = ldy;
+  p.partial = partial;
+  p.sem = sem;
+  p.dbg = env_dbg("TL_TCD_DBG");
+  if (getenv("TL_TRACE")) {
+    if (!g_trace) cudaMalloc(&g_trace, 16 * 256 * sizeof(long long));
+    p.trace = g_trace;
+  }
+  const uint32_t wb = (uint32_t)tile_bytes(w.bits);
+  p.w_off = 0;
+  p.s_off = p.w_off + wb;
+  p.z_off = p.s_off + 256;
+  p.a_off = p.z_off + 256;
+  p.stage_bytes = (p.a_off + 127) & ~127u;
+  const uint32_t red = (uint32_t)kTcdNG * (uint32_t)M * kBN * 4;
+  const uint32_t opb = kTcdNOP * kTcdOpBytes;
+  const uint32_t sums = (uint32_t)(K / kBK) * (M <= 1 ? 1u : (uint32_t)kTcdNB) * 4;
+  const uint32_t fixed = 1024 /*align*/ + opb + 1024 + red + sums + 1024 /*barriers, tmem slot, flags*/;
+  int ns = (int)((227u * 1024u - fixed) / p.stage_bytes);
+  if (ns > 32) ns = 32;
+  if (env_dbg("TL_TCD_NS") > 0 && env_dbg("TL_TCD_NS") < ns) ns = env_dbg("TL_TCD_NS");
+  if (ns < kTcdNOP) return fail(TL_EUNSUPPORTED, "decode tensor-core stage does not fit shared memory");
+  p.ns = ns;
+  p.op_off = ((uint32_t)ns * p.stage_bytes + 1023) & ~1023u;
+  p.red_off = p.op_off + opb;
+  p.sums_off = p.red_off + red;
+  p.bar_off = (p.sums_off + sums + 15) & ~15u;
+  const uint32_t smem = p.bar_off + (3 * ns + kTcdNOP + 2 * kTcdNW + 2 * kTcdNACC) * 8 + 32 + 1024;
+  if (smem > 227 * 1024) return fail(TL_EUNSUPPORTED, "decode tensor-core tile does not fit shared memory");
+  int grid = grid_req > 0 ? grid_req : sms;
+  if (grid > 160) grid = 160;
+  if (grid > p.units) grid = p.units;
+  CUtensorMap tmap;
+  tl_status s = make_tmap_a(&tmap, A, M, K, lda, kTcdNB);
+  if (s != TL_OK) return s;
+  s = TL_EUNSUPPORTED;
+  dispatch_format(w.kind, w.bits, w.kind == 2 ? w.exp_bits : 0, [&](auto f) {
+    using F = decltype(f);
+    s = launch_tcd<F>(p, &tmap, grid, smem, st);
+  });
+  return s;
+}
 
 size_t tcs_workspace_bytes(int64_t M, int64_t N, int64_t K) {
   (void)M;
@@ -33,6 +107,7 @@ size_t tcs_workspace_bytes(int64_t M, int64_t N, int64_t K) {
 tl_status tcs_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, const __half* A, int64_t lda,
                      const uint8_t* wt, const __half* scales, const __half* zeros, __half* Y, int64_t ldy,
                      float* partial, int* sem, int grid_req, cudaStream_t st) {
+  if (!getenv("TL_TCS_V1")) return tcd_matmul(w, M, N, K, G, A, lda, wt, scales, zeros, Y, ldy, partial, sem, grid_req, st);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

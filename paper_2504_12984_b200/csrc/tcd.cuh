@@ -1,0 +1,537 @@
+// tcd.cuh -- decode-batch tensor-core path (M <= 16, group a multiple of 128): SURVEY §8(a)
+// rows a3-a11 for the HBM-bound regime ("for small batch sizes the primary
+// bottleneck is loading weights from global memory to registers").
+//
+// Swap-AB tcgen05.mma.cta_group::1.kind::f16: M_mma = 128 weight columns (the dequantized W^T
+// tile, written to TENSOR MEMORY with tcgen05.st -- the "TS" form), N_mma = 16 batch rows (the
+// activation operand, 128B-swizzled K-major in shared memory), fp32 accumulation in TMEM
+// (PAPER.md:191).  The per-weight work is the unpack alone:
+//
+//  * an integer code u placed at bit P of each 16-bit half IS the fp16 u * 2^(P-24) (exact:
+//    fp16 subnormals are multiplied exactly by the tensor core), so the dequant is one AND (plus
+//    one shared SHF per word) per PAIR of weights -- no conversion, no zero-point subtraction;
+//    the activation operand is pre-scaled by 2^-P per k, so the MMA accumulates
+//    D = 2^-24 sum_k A[m,k] u[k,n]; ints are stored offset-binary (zero point 2^(b-1));
+//  * the zero point and the group scale are applied once per (tile, column, batch row) in fp32:
+//        Y[m,n] += s[g,n] * (2^24 * D[n,m] - z[g,n] * sum_{k in tile} A[m,k])
+//    where the activation sums are computed once per tile by the preparation warps;
+//  * float codes are placed on the fp16 exponent/mantissa fields (value * 2^(bias-15), exact)
+//    and Y += s * 2^(15-bias) * D.
+//
+// Everything a tile needs -- the packed weight tile (2048*b B), its scale and zero-point row
+// slices (256 B each) and the M activation row slices (256 B each) -- arrives in ONE TMA ring
+// stage (cp.async.bulk, PAPER.md:148-151 step (1)), so no thread ever waits on a long-latency
+// global load.  Roles (128 + 128*NG threads):
+//   warp 0       TMA producer (one elected thread)
+//   warp 1       TMEM allocator + MMA issuer (one elected thread)
+//   warps 2..3   preparation: per stage, sum_k A per row and the pre-scaled swizzled operand
+//   warps 4..    NG dequant groups of 4 warps (warp%4 = TMEM lane quarter = 32 columns); group
+//                g handles tiles t = g, g+NG, ... of the CTA's stream-K range: unpack into its
+//                W^T slot, hand it to the MMA, then -- one group-iteration late, so it never waits
+//                for its own MMA -- read the tile's accumulator and apply the fp32 fixup.
+// Stream-K: the linear unit space u = nt*KT + kt is cut into `grid` contiguous
+// ranges; n-tiles shared by several CTAs are reduced in fixed CTA order (reading R12).
+#pragma once
+
+#include <cuda.h>
+
+#include "paths.cuh"
+#include "ptx.cuh"
+
+namespace tl {
+
+struct TcdParams {
+  int M, N, K, G;
+  int units;
+  int ns;                          // TMA ring stages
+  uint32_t stage_bytes;            // [weight tile | scale 256 | zero 256 | A M*256 | sums 64]
+  uint32_t w_off, s_off, z_off, a_off;
+  uint32_t sums_off;  // [K/128][MT] fp32: sum_k A[m,k] over every 128-k tile (ints only)
+  uint32_t op_off, red_off, bar_off;  // operand ring [kTcdNOP][4 KB] (1024-aligned), reduction, barriers
+  const uint8_t* wt;
+  const __half* A;
+  int64_t lda;
+  const __half* scales;
+  const __half* zeros;
+  __half* Y;
+  int64_t ldy;
+  float* partial;  // [grid][2][16][128] fp32
+  int* sem;
+  long long* trace;  // optional [grid][16] %globaltimer stamps (TL_TRACE)
+  int dbg;  // debug knobs (TL_TCD_DBG): 1 skip MMAs, 2 skip prep arithmetic, 4 skip unpack/STTM
+};
+
+constexpr int kTcdNG = 4;                       // dequant groups
+constexpr int kTcdNW = 5;                       // W^T TMEM slots (64 columns each), slot = tile % 5
+constexpr int kTcdNACC = 12;                    // accumulator slots (16 TMEM columns each): 5*64 + 12*16 = 512
+constexpr int kTcdThreads = 128 + kTcdNG * 128;
+constexpr int kTcdNB = 16;                      // MMA N (batch rows, zero-padded)
+constexpr uint32_t kTcdOpBytes = kTcdNB * 256;  // 16 rows x 128 k fp16, two 64-k SW128 blocks
+constexpr uint32_t kTcdAccCol = 64 * kTcdNW;
+constexpr int kTcdNOP = 8;                      // activation operand ring slots
+constexpr int kTcdNPREP = 1;                    // preparation warps (alternate tiles)
+
+__device__ __forceinline__ void tcd_sttm_x16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ uint32_t tcd_ldtm_x1(uint32_t taddr) {
+  uint32_t r;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
+  return r;
+}
+// D[tmem] (+)= A[tmem] * B[smem], kind::f16
+__device__ __forceinline__ void tcd_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// shared-memory matrix descriptor: K-major, 128B swizzle, 8-row groups 1024 B apart
+__device__ __forceinline__ uint64_t tcd_sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t x) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(x) : "memory");
+}
+__device__ __forceinline__ void sts64(uint32_t a, uint32_t x, uint32_t y) {
+  asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(a), "r"(x), "r"(y) : "memory");
+}
+
+// segment words of column n of a transformed tile in shared memory
+template <int B>
+__device__ __forceinline__ void tcd_load_words(uint32_t wtile, int n, uint32_t* words) {
+#pragma unroll
+  for (int s = 0; s < num_segs(B); ++s) {
+    const int w = seg_width(B, s), base = seg_base(B, s);
+#pragma unroll
+    for (int v = 0; v < w; ++v) {
+      const uint4 x = lds128(wtile + 2048 * base + (v * 128 + n) * 16);
+      words[4 * base + 4 * v + 0] = x.x;
+      words[4 * base + 4 * v + 1] = x.y;
+      words[4 * base + 4 * v + 2] = x.z;
+      words[4 * base + 4 * v + 3] = x.w;
+    }
+  }
+}
+
+__device__ __forceinline__ void tcd_stamp(const TcdParams& p, int i) {
+  if (p.trace != nullptr) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[blockIdx.x * 16 + i] = t;
+  }
+}
+
+// per-iteration clock64 stamps of CTA 0, group 0, warp 0, lane 0 (TL_TRACE): [iter][8] at 2400
+__device__ __forceinline__ void tcd_istamp(const TcdParams& p, int dw, int lane, uint32_t kk, int i) {
+  if (p.trace != nullptr && blockIdx.x == 0 && dw == 0 && lane == 0 && kk < 40) p.trace[2400 + kk * 8 + i] = clock64();
+}
+
+template <class F, int MT>
+__global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_constant__ CUtensorMap tmapA, TcdParams p) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  constexpr bool kInt = F::kind != kFloat;  // integer codes: pre-scaled operand + zero-point term
+  constexpr uint32_t WB = tile_bytes(F::bits);
+  constexpr int NG = kTcdNG, NACC = kTcdNACC;
+  const int NS = p.ns;
+  const uint32_t SB = p.stage_bytes;
+  const uint32_t st_u = smem_u32(smem);
+  float* red = reinterpret_cast<float*>(smem + p.red_off);  // [NG][M][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bar_off);
+  uint64_t* full_tma = bars;               // [NS] stage landed
+  uint64_t* full_op = bars + NS;           // [NOP] activation operand landed (NS >= NOP)
+  uint64_t* empty_tma = bars + 2 * NS;     // [NS] group read the stage
+  uint64_t* empty_op = bars + 3 * NS;      // [NOP] MMA done with the operand slot
+  uint64_t* full_w = empty_op + kTcdNOP;   // [NW] W^T slot written
+  uint64_t* empty_w = full_w + kTcdNW;     // [NW] MMA done with the W^T slot
+  uint64_t* full_acc = empty_w + kTcdNW;   // [NACC] accumulator ready
+  uint64_t* empty_acc = full_acc + NACC;   // [NACC] accumulator read back
+  uint32_t* tslot_ptr = reinterpret_cast<uint32_t*>(empty_acc + NACC);
+  int* flag = reinterpret_cast<int*>(tslot_ptr + 4);
+
+  const int KT = p.K / kBK;
+  const int grid = gridDim.x;
+  const int cta = blockIdx.x;
+  const int u0 = (int)((int64_t)cta * p.units / grid);
+  const int u1 = (int)((int64_t)(cta + 1) * p.units / grid);
+  const int T = u1 - u0;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const bool has_zeros = F::kind == kUint && p.zeros != nullptr;
+
+  if (threadIdx.x == 0) {
+    tcd_stamp(p, 0);
+    if (p.trace) p.trace[blockIdx.x * 16 + 10] = T;
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full_tma[s], 1);
+      mbar_init(&empty_tma[s], 4);
+    }
+    for (int i = 0; i < kTcdNOP; ++i) {
+      mbar_init(&empty_op[i], 1);
+      mbar_init(&full_op[i], 1);
+    }
+    for (int i = 0; i < kTcdNW; ++i) {
+      mbar_init(&full_w[i], 4);
+      mbar_init(&empty_w[i], 1);
+    }
+    for (int i = 0; i < NACC; ++i) {
+      mbar_init(&full_acc[i], 1);
+      mbar_init(&empty_acc[i], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tslot_ptr, 512);
+    tmem_relinquish();
+  }
+  // zero the activation operand ring once: rows >= M are never written again
+  const uint32_t op_u = st_u + p.op_off;
+  for (uint32_t i = threadIdx.x; i < kTcdNOP * kTcdOpBytes / 16; i += kTcdThreads) sts128(op_u + i * 16, 0u, 0u, 0u, 0u);
+  if constexpr (kInt) {
+    // sum_k A[m, k] of every 128-k tile (zero-point term), 4 (tile, row) pairs per warp in flight
+    float* sums_w = reinterpret_cast<float*>(smem + p.sums_off);
+    const int n_pairs = KT * p.M;
+    for (int i0 = warp * 4; i0 < n_pairs; i0 += (kTcdThreads / 32) * 4) {
+      uint2 v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int i = min(i0 + j, n_pairs - 1);
+        const int kt = i / p.M, m = i - (i / p.M) * p.M;
+        v[j] = __ldg(reinterpret_cast<const uint2*>(p.A + m * p.lda + (int64_t)kt * kBK) + lane);
+      }
+      float sm[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f0 = __half22float2(u32_as_h2(v[j].x)), f1 = __half22float2(u32_as_h2(v[j].y));
+        sm[j] = (f0.x + f0.y) + (f1.x + f1.y);
+      }
+#pragma unroll
+      for (int d = 16; d >= 1; d >>= 1)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sm[j] += __shfl_xor_sync(0xffffffffu, sm[j], d);
+      if (lane == 0)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int i = i0 + j;
+          if (i < n_pairs) sums_w[(i / p.M) * MT + (i - (i / p.M) * p.M)] = sm[j];
+        }
+    }
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot_ptr;
+  if (threadIdx.x == 0) tcd_stamp(p, 1);
+  const float* sums = reinterpret_cast<const float*>(smem + p.sums_off);
+
+  if (warp == 0 || warp == 2) {
+    // ------------------------------ TMA producers ------------------------------
+    // warp 0: the stage = packed weight tile + its scale / zero-point row slices (HBM streams,
+    // gated only by the stage ring); warp 2: the activation operand of the tile (two 64-k x 16-row
+    // boxes from L2, 128B-swizzled by the TMA unit, rows >= M zero-filled), gated by the operand
+    // ring that the MMA releases.  Separate issuers keep the weight stream from ever waiting on
+    // the MMA.
+    if (elect_one()) {
+      const uint64_t pol_first = policy_evict_first();
+      const uint64_t pol_last = policy_evict_last();
+      int nt = u0 / KT, kt = u0 - (u0 / KT) * KT;
+      if (warp == 0) {
+        const bool side = !(p.dbg & 8);
+        const uint32_t bytes = WB + (side ? 256u + (has_zeros ? 256u : 0u) : 0u);
+        const uint32_t bar0 = smem_u32(full_tma);
+        const uint8_t* src = p.wt + (int64_t)u0 * WB;
+        const int tpg = p.G / kBK;  // k-tiles per group
+        int grow = kt / tpg, grem = kt - (kt / tpg) * tpg;
+        int s = 0;
+        uint32_t ph = 0;
+        for (int t = 0; t < T; ++t) {
+          if (t >= NS) mbar_wait(&empty_tma[s], ph ^ 1);
+          if (p.trace && blockIdx.x == 0 && t < 64) p.trace[2720 + t] = clock64();
+          const uint32_t st = st_u + s * SB, bar = bar0 + 8 * s;
+          mbar_arrive_expect_tx_u32(bar, bytes);
+          tma_bulk_g2s_cta(st + p.w_off, src, WB, bar, pol_first);
+          if (side) {
+            const int64_t so = (int64_t)grow * p.N + (int64_t)nt * kBN;
+            tma_bulk_g2s_cta(st + p.s_off, p.scales + so, 256, bar, pol_first);
+            if (has_zeros) tma_bulk_g2s_cta(st + p.z_off, p.zeros + so, 256, bar, pol_first);
+          }
+          if (t == 0) tcd_stamp(p, 2);
+          if (t == T - 1) tcd_stamp(p, 3);
+          src += WB;
+          if (++kt == KT) {
+            kt = 0;
+            ++nt;
+            grow = 0;
+            grem = 0;
+          } else if (++grem == tpg) {
+            grem = 0;
+            ++grow;
+          }
+          if (++s == NS) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      } else {
+        prefetch_tmap(&tmapA);
+        int o = 0;
+        uint32_t pho = 0;
+        for (int t = 0; t < T; ++t) {
+          if (t >= kTcdNOP) mbar_wait(&empty_op[o], pho ^ 1);
+          uint8_t* opp = smem + p.op_off + o * kTcdOpBytes;
+          mbar_arrive_expect_tx(&full_op[o], kTcdOpBytes);
+          tma_load_2d(opp, &tmapA, kt * kBK, 0, &full_op[o], pol_last);
+          tma_load_2d(opp + kTcdNB * 128, &tmapA, kt * kBK + 64, 0, &full_op[o], pol_last);
+          if (++kt == KT) kt = 0;
+          if (++o == kTcdNOP) {
+            o = 0;
+            pho ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------ MMA issuer (one thread) ------------------------------
+    // the dequant group has already seen the tile's activation operand land (full_op) before it
+    // arrives on full_w, so the issuer waits only for the W^T slot and the accumulator
+    if (elect_one()) {
+      const uint32_t idesc = (1u << 4) | ((uint32_t)(kTcdNB >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+      int o = 0, g = 0, a = 0;
+      uint32_t kk = 0, ka = 0;  // t / NW, t / NACC
+      for (int t = 0; t < T; ++t) {
+        mbar_wait(&full_w[g], kk & 1);
+        if (p.trace && blockIdx.x == 0 && t < 64) p.trace[2976 + 3 * t] = clock64();
+        if (t >= NACC) mbar_wait(&empty_acc[a], (ka - 1) & 1);
+        if (p.trace && blockIdx.x == 0 && t < 64) p.trace[2977 + 3 * t] = clock64();
+        tc_fence_after();
+        const uint64_t bd = tcd_sw128_desc(op_u + o * kTcdOpBytes);
+        const uint32_t d = tmem + kTcdAccCol + a * kTcdNB;
+        const uint32_t aw = tmem + g * 64;
+        if (!(p.dbg & 1))
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          tcd_mma_ts(d, aw + j * 8, bd + (uint64_t)((j >> 2) * (kTcdNB * 128 / 16) + (j & 3) * 2), idesc,
+                     j > 0 ? 1u : 0u);
+        tc_commit(&empty_w[g]);
+        tc_commit(&full_acc[a]);
+        tc_commit(&empty_op[o]);
+        if (p.trace && blockIdx.x == 0 && t < 64) p.trace[2978 + 3 * t] = clock64();
+        if (t == T - 1) tcd_stamp(p, 8);
+        if (++o == kTcdNOP) o = 0;
+        if (++g == kTcdNW) {
+          g = 0;
+          ++kk;
+        }
+        if (++a == NACC) {
+          a = 0;
+          ++ka;
+        }
+      }
+    }
+  } else if (warp == 3) {
+    // spare warp (keeps the dequant warps aligned to TMEM lane quarters)
+  } else {
+    // ------------------------------ dequant groups ------------------------------
+    const int dw = warp - 4;
+    const int g = dw >> 2;
+    const int q = warp & 3;
+    const int n = q * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    int wsl = g;          // W^T slot of the current tile (t % NW) and its lap (t / NW)
+    uint32_t lapw = 0;
+    const float c1mul = kInt ? 16777216.f : (float)(1 << (15 - F::bias));
+    float tot[MT];
+#pragma unroll
+    for (int m = 0; m < MT; ++m) tot[m] = 0.f;
+
+    auto fixup = [&](int tp, float c1) {
+      const int a = tp % NACC;
+      mbar_wait(&full_acc[a], (uint32_t)(tp / NACC) & 1);
+      tc_fence_after();
+      const uint32_t ta = tmem + lane_off + kTcdAccCol + a * kTcdNB;
+      if constexpr (MT == 1) {
+        const uint32_t d = tcd_ldtm_x1(ta);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_acc[a]);
+        tot[0] = fmaf(c1, __uint_as_float(d), tot[0]);
+      } else {
+        uint32_t d[16];
+        tmem_ld_32x32b_x16(ta, d);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_acc[a]);
+#pragma unroll
+        for (int m = 0; m < MT; ++m) tot[m] = fmaf(c1, __uint_as_float(d[m]), tot[m]);
+      }
+    };
+
+    int t = g;
+    int s = g % NS;
+    uint32_t ph = (uint32_t)(g / NS) & 1;
+    uint32_t kk = 0;   // this group's tile counter
+    // the fixup of a tile is applied two group-iterations late, so the in-order MMA issuer has
+    // reached it by then: tp2 (older) and tp1 are pending, with their scale * c1mul
+    int tp1 = -1, tp2 = -1;
+    float c1p1 = 0.f, c1p2 = 0.f;
+    int t0 = 0;
+    while (t0 < T) {
+      const int ufirst = u0 + t0;
+      const int nt = ufirst / KT;
+      const int t1 = min(T, t0 + (KT - (ufirst - nt * KT)));
+      for (; t < t1; t += NG, ++kk) {
+        tcd_istamp(p, dw, lane, kk, 0);
+        mbar_wait(&full_tma[s], ph);
+        tcd_istamp(p, dw, lane, kk, 1);
+        if (kk == 0 && dw == 0 && lane == 0) tcd_stamp(p, 4);
+        const uint32_t st = st_u + s * SB;
+        uint32_t words[4 * F::bits];
+        tcd_load_words<F::bits>(st + p.w_off, n, words);
+        const float sc = __half2float(__ushort_as_half(lds16(st + p.s_off + 2 * n)));
+        if constexpr (kInt) {
+          float z = (float)(1 << (F::bits - 1));
+          if constexpr (F::kind == kUint) z = has_zeros ? __half2float(__ushort_as_half(lds16(st + p.z_off + 2 * n))) : 0.f;
+          const float c2 = -sc * z;
+          const float* sa = sums + (u0 + t - nt * KT) * MT;
+#pragma unroll
+          for (int m = 0; m < MT; ++m) tot[m] = fmaf(c2, sa[m], tot[m]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_tma[s]);
+        tcd_istamp(p, dw, lane, kk, 2);
+        if (t >= kTcdNW) mbar_wait(&empty_w[wsl], (lapw - 1) & 1);
+        const uint32_t tslot = tmem + lane_off + wsl * 64;
+        tcd_istamp(p, dw, lane, kk, 3);
+        if (!(p.dbg & 4)) static_for<0, 4>([&](auto CC) {
+          constexpr int c = decltype(CC)::value;
+          uint32_t r[16];
+          static_for<0, 16>([&](auto II) {
+            constexpr int ii = decltype(II)::value;
+            if constexpr (kInt) r[ii] = assemble_pair<F::bits, c * 16 + ii, 0>(words);  // u * 2^-24
+            else r[ii] = raw_pair_bits<F, c * 16 + ii>(words);
+          });
+          tcd_sttm_x16(tslot + c * 16, r);
+        });
+        tcd_istamp(p, dw, lane, kk, 4);
+        tmem_st_wait();
+        tcd_istamp(p, dw, lane, kk, 5);
+        mbar_wait(&full_op[t % kTcdNOP], (uint32_t)(t / kTcdNOP) & 1);  // the tile's activation operand landed
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full_w[wsl]);
+        wsl += NG;
+        while (wsl >= kTcdNW) {
+          wsl -= kTcdNW;
+          ++lapw;
+        }
+        if (tp2 >= 0) fixup(tp2, c1p2);
+        tp2 = tp1;
+        c1p2 = c1p1;
+        tcd_istamp(p, dw, lane, kk, 6);
+        tp1 = t;
+        c1p1 = sc * c1mul;
+        s += NG;
+        while (s >= NS) {
+          s -= NS;
+          ph ^= 1;
+        }
+      }
+      if (dw == 0 && lane == 0) tcd_stamp(p, 5);
+      if (tp2 >= 0) fixup(tp2, c1p2);
+      if (tp1 >= 0) fixup(tp1, c1p1);
+      tp1 = tp2 = -1;
+      if (dw == 0 && lane == 0) tcd_stamp(p, 6);
+      // ---- n-tile nt done by this CTA: sum the groups' totals, write Y or a stream-K partial ----
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+        if (m < p.M) red[(g * p.M + m) * kBN + n] = tot[m];
+      named_bar_sync(1, NG * 128);
+      const int ua = nt * KT, ub = ua + KT;
+      const bool complete = (u0 <= ua) && (u1 >= ub);
+      const int col = nt * kBN + n;
+      const int slot2 = (nt == u0 / KT) ? 0 : 1;
+      float* part = p.partial + ((int64_t)(cta * 2 + slot2) * kTcdNB) * kBN;
+      for (int m = g; m < p.M; m += NG) {
+        float v = 0.f;
+#pragma unroll
+        for (int gg = 0; gg < NG; ++gg) v += red[(gg * p.M + m) * kBN + n];
+        if (complete) p.Y[(int64_t)m * p.ldy + col] = __float2half_rn(v);
+        else __stcg(part + (int64_t)m * kBN + n, v);
+      }
+      if (!complete) {
+        __threadfence();
+        named_bar_sync(1, NG * 128);
+        if (threadIdx.x == 128) {
+          const int lo = (int)((((int64_t)ua + 1) * grid - 1) / p.units);
+          const int hi = (int)((((int64_t)ub) * grid - 1) / p.units);
+          const int prev = atomicAdd(&p.sem[nt], 1);
+          flag[0] = (prev == hi - lo) ? 1 : 0;
+          flag[1] = lo;
+          flag[2] = hi;
+        }
+        named_bar_sync(1, NG * 128);
+        if (flag[0]) {
+          __threadfence();
+          const int lo = flag[1], hi = flag[2];
+          for (int m = g; m < p.M; m += NG) {
+            float sum = 0.f;
+            for (int qq = lo; qq <= hi; ++qq) {
+              const int q_first = (int)((int64_t)qq * p.units / grid) / KT;
+              const int qslot = (nt == q_first) ? 0 : 1;
+              sum += __ldcg(p.partial + ((int64_t)(qq * 2 + qslot) * kTcdNB + m) * kBN + n);
+            }
+            p.Y[(int64_t)m * p.ldy + col] = __float2half_rn(sum);
+          }
+          if (threadIdx.x == 128) p.sem[nt] = 0;
+        }
+      }
+      named_bar_sync(1, NG * 128);
+      if (dw == 0 && lane == 0) tcd_stamp(p, 9);
+#pragma unroll
+      for (int m = 0; m < MT; ++m) tot[m] = 0.f;
+      t0 = t1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+  if (threadIdx.x == 0) tcd_stamp(p, 7);
+}
+
+template <class F, int MT>
+tl_status launch_tcd_mt(const TcdParams& p, const CUtensorMap* tmap, int grid, uint32_t smem_bytes, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(tcd_kernel<F, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
+        cudaSuccess)
+      return fail(TL_ECUDA, "cudaFuncSetAttribute(tcd smem)");
+    configured = true;
+  }
+  tcd_kernel<F, MT><<<grid, kTcdThreads, smem_bytes, st>>>(*tmap, p);
+  return check_launch("tcd_kernel");
+}
+
+template <class F>
+tl_status launch_tcd(const TcdParams& p, const CUtensorMap* tmap, int grid, uint32_t smem_bytes, cudaStream_t st) {
+  return p.M <= 1 ? launch_tcd_mt<F, 1>(p, tmap, grid, smem_bytes, st)
+                  : launch_tcd_mt<F, kTcdNB>(p, tmap, grid, smem_bytes, st);
+}
+
+}  // namespace tl
