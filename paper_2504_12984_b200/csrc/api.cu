@@ -36,8 +36,8 @@ static int choose_path(tl_wtype w, int64_t M, int32_t G) {
   (void)w;
   // measured on B200: the CUDA-core path is fastest at M = 1, the
   // tensor-memory decode variant for 2 <= M <= 16 (group >= 128), the smem variant otherwise
-  if (M <= 1) return TL_PATH_GEMV;
   if (tcs_eligible(M, G)) return TL_PATH_TCS;
+  if (M <= 1) return TL_PATH_GEMV;
   return TL_PATH_TC;
 }
 

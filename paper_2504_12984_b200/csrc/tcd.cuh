@@ -198,46 +198,52 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
     tmem_alloc(tslot_ptr, 512);
     tmem_relinquish();
   }
-  // zero the activation operand ring once: rows >= M are never written again
   const uint32_t op_u = st_u + p.op_off;
-  for (uint32_t i = threadIdx.x; i < kTcdNOP * kTcdOpBytes / 16; i += kTcdThreads) sts128(op_u + i * 16, 0u, 0u, 0u, 0u);
-  if constexpr (kInt) {
-    // sum_k A[m, k] of every 128-k tile (zero-point term), 4 (tile, row) pairs per warp in flight
-    float* sums_w = reinterpret_cast<float*>(smem + p.sums_off);
-    const int n_pairs = KT * p.M;
-    for (int i0 = warp * 4; i0 < n_pairs; i0 += (kTcdThreads / 32) * 4) {
-      uint2 v[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int i = min(i0 + j, n_pairs - 1);
-        const int kt = i / p.M, m = i - (i / p.M) * p.M;
-        v[j] = __ldg(reinterpret_cast<const uint2*>(p.A + m * p.lda + (int64_t)kt * kBK) + lane);
-      }
-      float sm[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float2 f0 = __half22float2(u32_as_h2(v[j].x)), f1 = __half22float2(u32_as_h2(v[j].y));
-        sm[j] = (f0.x + f0.y) + (f1.x + f1.y);
-      }
-#pragma unroll
-      for (int d = 16; d >= 1; d >>= 1)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) sm[j] += __shfl_xor_sync(0xffffffffu, sm[j], d);
-      if (lane == 0)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int i = i0 + j;
-          if (i < n_pairs) sums_w[(i / p.M) * MT + (i - (i / p.M) * p.M)] = sm[j];
-        }
-    }
-  }
-  fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot_ptr;
   if (threadIdx.x == 0) tcd_stamp(p, 1);
   const float* sums = reinterpret_cast<const float*>(smem + p.sums_off);
+  // Programmatic dependent launch: the weight stream (warp 0) depends on nothing the previous
+  // kernel in the stream writes, so it starts right away; every other warp waits for the previous
+  // grid (it may have produced A, or still use Y / the workspace) before touching them.
+  if (warp == 0) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  } else {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if constexpr (kInt) {
+      // sum_k A[m, k] of every 128-k tile (zero-point term), 4 (tile, row) pairs per warp in flight
+      float* sums_w = reinterpret_cast<float*>(smem + p.sums_off);
+      const int n_pairs = KT * p.M;
+      for (int i0 = (warp - 1) * 4; i0 < n_pairs; i0 += (kTcdThreads / 32 - 1) * 4) {
+        uint2 v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int i = min(i0 + j, n_pairs - 1);
+          const int kt = i / p.M, m = i - (i / p.M) * p.M;
+          v[j] = __ldg(reinterpret_cast<const uint2*>(p.A + m * p.lda + (int64_t)kt * kBK) + lane);
+        }
+        float sm[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f0 = __half22float2(u32_as_h2(v[j].x)), f1 = __half22float2(u32_as_h2(v[j].y));
+          sm[j] = (f0.x + f0.y) + (f1.x + f1.y);
+        }
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) sm[j] += __shfl_xor_sync(0xffffffffu, sm[j], d);
+        if (lane == 0)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int i = i0 + j;
+            if (i < n_pairs) sums_w[(i / p.M) * MT + (i - (i / p.M) * p.M)] = sm[j];
+          }
+      }
+    }
+    named_bar_sync(2, kTcdThreads - 32);  // sums visible to the dequant groups
+  }
 
   if (warp == 0 || warp == 2) {
     // ------------------------------ TMA producers ------------------------------
@@ -524,7 +530,18 @@ tl_status launch_tcd_mt(const TcdParams& p, const CUtensorMap* tmap, int grid, u
       return fail(TL_ECUDA, "cudaFuncSetAttribute(tcd smem)");
     configured = true;
   }
-  tcd_kernel<F, MT><<<grid, kTcdThreads, smem_bytes, st>>>(*tmap, p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kTcdThreads);
+  cfg.dynamicSmemBytes = smem_bytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tcd_kernel<F, MT>, *tmap, p);
+  if (e != cudaSuccess) return fail(TL_ECUDA, "tcd_kernel launch: %s", cudaGetErrorString(e));
   return check_launch("tcd_kernel");
 }
 

@@ -132,3 +132,46 @@ def test_matmul_full_size_sampled_columns(env, fmt, layer):
         w = dequant(parse_wtype(fmt), codes[:, cols], s[:, cols], None if z is None else z[:, cols], G)
         r = tolerance_check(Y[:, cols], Y64, A, w)
         assert r["ok"], r
+
+
+@pytest.mark.parametrize("graph", [False, True])
+@pytest.mark.parametrize("fmt", ["u4", "i5", "f6e3m2"])
+def test_dependent_chain_programmatic_launch(env, fmt, graph):
+    """The decode path is launched with programmatic dependent launch: its weight stream starts
+    before the previous kernel finishes, everything that reads A or writes Y / the workspace waits
+    (griddepcontrol.wait).  Chain Y1 = A W1, Y2 = Y1 W2, Y3 = Y2 W3 back to back on one stream
+    (eager and captured in a CUDA graph), with one shared workspace: each step must match the
+    oracle applied to the GPU's own previous output."""
+    P, torch = env
+    M, K, G = 1, 2048, 128
+    A, _, _, _ = make_problem(fmt, M, K, K, G, seed_tag="chain")
+    ws = torch.zeros(64 << 20, dtype=torch.uint8, device="cuda")
+    layers = []
+    for i in range(3):
+        _, codes, s, z = make_problem(fmt, M, K, K, G, seed_tag=f"chain{i}")
+        w, _, wt = prepare_weights(P, torch, fmt, K, K, codes)
+        layers.append((codes, s, z, w, wt, to_dev(s, torch), to_dev(z, torch)))
+    X = [to_dev(A, torch)] + [torch.full((M, K), float("nan"), dtype=torch.float16, device="cuda") for _ in range(3)]
+
+    def chain():
+        for i, (_, _, _, w, wt, s_d, z_d) in enumerate(layers):
+            P.tl_matmul(w, M, K, K, G, X[i], wt, s_d, z_d, X[i + 1], ws)
+
+    if graph:
+        chain()
+        torch.cuda.synchronize()
+        for x in X[1:]:
+            x.fill_(float("nan"))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            chain()
+        g.replay()
+    else:
+        chain()
+    torch.cuda.synchronize()
+    for i, (codes, s, z, *_rest) in enumerate(layers):
+        Ain = X[i].cpu().numpy().astype(np.float16)
+        Yi = X[i + 1].cpu().numpy()
+        assert not np.isnan(Yi).any()
+        _check(fmt, Ain, codes, s, z, G, Yi)
+    assert int(ws[:65536].view(torch.int32).abs().sum()) == 0
