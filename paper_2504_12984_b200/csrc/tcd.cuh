@@ -158,7 +158,11 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
   uint64_t* empty_op = bars + 3 * NS;      // [NOP] MMA done with the operand slot
   uint64_t* full_w = empty_op + kTcdNOP;   // [NW] W^T slot written
   uint64_t* empty_w = full_w + kTcdNW;     // [NW] MMA done with the W^T slot
-  uint64_t* full_acc = empty_w + kTcdNW;   // [NACC] accumulator ready
+  // [NACC] "MMA(t) complete" (one tcgen05.commit per tile, slot t % NACC).  It also frees the W^T
+  // slot and the operand slot of tile t.  No accumulator-empty barrier is needed: the fixup of
+  // tile t - NACC is done by the same group (NACC % NG == 0) before it arrives on full_w for t.
+  // Every waiter for MMA(j) provably waits before MMA(j + NACC) can complete (parity is safe).
+  uint64_t* full_acc = empty_w + kTcdNW;
   uint64_t* empty_acc = full_acc + NACC;   // [NACC] accumulator read back
   uint32_t* tslot_ptr = reinterpret_cast<uint32_t*>(empty_acc + NACC);
   int* flag = reinterpret_cast<int*>(tslot_ptr + 4);
@@ -298,7 +302,8 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
         int o = 0;
         uint32_t pho = 0;
         for (int t = 0; t < T; ++t) {
-          if (t >= kTcdNOP) mbar_wait(&empty_op[o], pho ^ 1);
+          // operand slot t % NOP is free once MMA(t - NOP) completed (mma_done slot (t - NOP) % NACC)
+          if (t >= kTcdNOP) mbar_wait(&full_acc[(t - kTcdNOP) % NACC], (uint32_t)((t - kTcdNOP) / NACC) & 1);
           uint8_t* opp = smem + p.op_off + o * kTcdOpBytes;
           mbar_arrive_expect_tx(&full_op[o], kTcdOpBytes);
           tma_load_2d(opp, &tmapA, kt * kBK, 0, &full_op[o], pol_last);
@@ -322,7 +327,6 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
       for (int t = 0; t < T; ++t) {
         mbar_wait(&full_w[g], kk & 1);
         if (p.trace && blockIdx.x == 0 && t < 64) p.trace[2976 + 3 * t] = clock64();
-        if (t >= NACC) mbar_wait(&empty_acc[a], (ka - 1) & 1);
         if (p.trace && blockIdx.x == 0 && t < 64) p.trace[2977 + 3 * t] = clock64();
         tc_fence_after();
         const uint64_t bd = tcd_sw128_desc(op_u + o * kTcdOpBytes);
@@ -333,9 +337,7 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
         for (int j = 0; j < 8; ++j)
           tcd_mma_ts(d, aw + j * 8, bd + (uint64_t)((j >> 2) * (kTcdNB * 128 / 16) + (j & 3) * 2), idesc,
                      j > 0 ? 1u : 0u);
-        tc_commit(&empty_w[g]);
-        tc_commit(&full_acc[a]);
-        tc_commit(&empty_op[o]);
+        tc_commit(&full_acc[a]);  // "MMA(t) complete": frees W^T slot t%NW, operand slot t%NOP, fills acc t%NACC
         if (p.trace && blockIdx.x == 0 && t < 64) p.trace[2978 + 3 * t] = clock64();
         if (t == T - 1) tcd_stamp(p, 8);
         if (++o == kTcdNOP) o = 0;
@@ -375,7 +377,6 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty_acc[a]);
         tot[0] = fmaf(c1, __uint_as_float(d), tot[0]);
       } else {
         uint32_t d[16];
@@ -383,7 +384,6 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty_acc[a]);
 #pragma unroll
         for (int m = 0; m < MT; ++m) tot[m] = fmaf(c1, __uint_as_float(d[m]), tot[m]);
       }
@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_tma[s]);
         tcd_istamp(p, dw, lane, kk, 2);
-        if (t >= kTcdNW) mbar_wait(&empty_w[wsl], (lapw - 1) & 1);
+        if (t >= kTcdNW) mbar_wait(&full_acc[(t - kTcdNW) % NACC], (uint32_t)((t - kTcdNW) / NACC) & 1);
         const uint32_t tslot = tmem + lane_off + wsl * 64;
         tcd_istamp(p, dw, lane, kk, 3);
         if (!(p.dbg & 4)) static_for<0, 4>([&](auto CC) {
