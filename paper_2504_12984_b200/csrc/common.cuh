@@ -253,4 +253,25 @@ __device__ __forceinline__ uint32_t raw_pair_bits(const uint32_t* words) {
   }
 }
 
+// Deterministic stream-K reduction (reading R12) of one output element of n-tile nt: the partial
+// tiles of CTAs lo..hi summed in CTA order.  CTA q keeps two partial slots (0: its first n-tile,
+// 1: its last); every q > lo starts inside nt (slot 0), only q == lo may have started earlier
+// (lo_slot).  The loads are independent and issued eight at a time; the sum order is fixed.
+__device__ __forceinline__ float streamk_sum(const float* partial, int lo, int hi, int lo_slot, int64_t slot_stride,
+                                             int64_t off) {
+  float sum = 0.f;
+  for (int q0 = lo; q0 <= hi; q0 += 8) {
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int q = q0 + j;
+      v[j] = q <= hi ? __ldcg(partial + (int64_t)(q * 2 + (q == lo ? lo_slot : 0)) * slot_stride + off) : 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (q0 + j <= hi) sum += v[j];
+  }
+  return sum;
+}
+
 }  // namespace tl

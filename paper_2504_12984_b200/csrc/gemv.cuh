@@ -294,18 +294,14 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvParams p) {
           flag[0] = (prev == hi - lo) ? 1 : 0;
           flag[1] = lo;
           flag[2] = hi;
+          flag[3] = ((int)((int64_t)lo * p.units / grid) / KT == cur_nt) ? 0 : 1;
         }
         named_bar_sync(2, kBN);
         if (flag[0]) {
           __threadfence();
           const int lo = flag[1], hi = flag[2];
           for (int m = 0; m < p.M; ++m) {
-            float sum = 0.f;
-            for (int q = lo; q <= hi; ++q) {
-              const int q_first = (int)((int64_t)q * p.units / grid) / KT;
-              const int qslot = (cur_nt == q_first) ? 0 : 1;
-              sum += __ldcg(p.partial + ((int64_t)(q * 2 + qslot) * p.M + m) * kBN + c);
-            }
+            const float sum = streamk_sum(p.partial, lo, hi, flag[3], (int64_t)p.M * kBN, (int64_t)m * kBN + c);
             p.Y[(int64_t)m * p.ldy + n] = __float2half_rn(sum);
           }
           if (c == 0) p.sem[cur_nt] = 0;  // leave the semaphore clean for the next call

@@ -8,15 +8,12 @@
 
 #include "tc2.cuh"
 #include "tcd.cuh"
-#include "tcs.cuh"
 
 namespace tl {
 
 template <class F>
 tl_status launch_tc2(const Tc2Params& p, const CUtensorMap* tmap, int grid, uint32_t smem_bytes, cudaStream_t st);
 
-template <class F>
-tl_status launch_tcs(const TcsParams& p, int grid, uint32_t smem_bytes, cudaStream_t st);
 
 template <class F>
 tl_status launch_tcd(const TcdParams& p, const CUtensorMap* tmap, int grid, uint32_t smem_bytes, cudaStream_t st);
@@ -27,7 +24,7 @@ long long* g_trace = nullptr;  // debug: clock64 stamps of CTA 0 (TL_TRACE=1)
 
 bool tc_available() { return true; }
 
-bool tcs_eligible(int64_t M, int32_t G) { return M >= 1 && M <= kTcsNB && G >= kBK; }
+bool tcs_eligible(int64_t M, int32_t G) { return M >= 1 && M <= kTcdNB && G >= kBK; }
 
 static int env_dbg(const char* name) {
   const char* v = getenv(name);
@@ -59,8 +56,9 @@ static tl_status tcd_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t
   p.sem = sem;
   p.dbg = env_dbg("TL_TCD_DBG");
   if (getenv("TL_TRACE")) {
-    if (!g_trace) cudaMalloc(&g_trace, 16 * 256 * sizeof(long long));
-    p.trace = g_trace;
+    static int launches = 0;  // two trace buffers, alternating per launch (back-to-back overlap)
+    if (!g_trace) cudaMalloc(&g_trace, 2 * 16 * 256 * sizeof(long long));
+    p.trace = g_trace + (launches++ & 1) * 16 * 256;
   }
   const uint32_t wb = (uint32_t)tile_bytes(w.bits);
   p.w_off = 0;
@@ -101,62 +99,13 @@ size_t tcs_workspace_bytes(int64_t M, int64_t N, int64_t K) {
   (void)M;
   (void)N;
   (void)K;
-  return (size_t)160 * 2 * kTcsNB * 128 * 4;
+  return (size_t)160 * 2 * kTcdNB * 128 * 4;
 }
 
 tl_status tcs_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, const __half* A, int64_t lda,
                      const uint8_t* wt, const __half* scales, const __half* zeros, __half* Y, int64_t ldy,
                      float* partial, int* sem, int grid_req, cudaStream_t st) {
-  if (!getenv("TL_TCS_V1")) return tcd_matmul(w, M, N, K, G, A, lda, wt, scales, zeros, Y, ldy, partial, sem, grid_req, st);
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (sms > 160) sms = 160;
-  TcsParams p{};
-  p.M = (int)M;
-  p.N = (int)N;
-  p.K = (int)K;
-  p.G = G;
-  p.units = (int)((N / kBN) * (K / kBK));
-  p.wt = wt;
-  p.A = A;
-  p.lda = lda;
-  p.scales = scales;
-  p.zeros = zeros;
-  p.Y = Y;
-  p.ldy = ldy;
-  p.partial = partial;
-  p.sem = sem;
-  if (getenv("TL_TRACE")) {
-    if (!g_trace) cudaMalloc(&g_trace, 16 * 256 * sizeof(long long));
-    p.trace = g_trace;
-  }
-  const uint32_t stage = (uint32_t)tile_bytes(w.bits);
-  const uint32_t red = (uint32_t)kTcsGroups * (uint32_t)M * kBN * 4;
-  const uint32_t budget = 227 * 1024 - 1024 - 512;
-  int ns = 32, lg = 5;
-  while (ns > 2 && kTcsWSlots * kTcsApBytes + (uint32_t)ns * stage + red + 16 * kTcsNB * 16 + 1024 > budget) {
-    ns >>= 1;
-    --lg;
-  }
-  p.ns = ns;
-  p.lg_ns = lg;
-  p.stage_bytes = stage;
-  p.ap_off = 0;
-  p.st_off = kTcsWSlots * kTcsApBytes;
-  p.red_off = p.st_off + ns * stage;
-  p.bar_off = (p.red_off + red + 15) & ~15u;
-  const uint32_t smem = p.bar_off + (2 * ns + 2 * kTcsWSlots + 16) * 8 + 32 + 1024;
-  if (smem > 227 * 1024) return fail(TL_EUNSUPPORTED, "decode tensor-core tile does not fit shared memory");
-  int grid = grid_req > 0 ? grid_req : sms;
-  if (grid > 160) grid = 160;
-  if (grid > p.units) grid = p.units;
-  tl_status s = TL_EUNSUPPORTED;
-  dispatch_format(w.kind, w.bits, w.kind == 2 ? w.exp_bits : 0, [&](auto f) {
-    using F = decltype(f);
-    s = launch_tcs<F>(p, grid, smem, st);
-  });
-  return s;
+  return tcd_matmul(w, M, N, K, G, A, lda, wt, scales, zeros, Y, ldy, partial, sem, grid_req, st);
 }
 
 constexpr int kTcMaxCtas = 160;
@@ -256,5 +205,5 @@ tl_status tc_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, cons
 // debug hook (not part of the public ABI): copy the CTA-0 pipeline stamps to the host
 extern "C" int tl__debug_trace(long long* host) {
   if (!tl::g_trace) return -1;
-  return (int)cudaMemcpy(host, tl::g_trace, 16 * 256 * sizeof(long long), cudaMemcpyDeviceToHost);
+  return (int)cudaMemcpy(host, tl::g_trace, 2 * 16 * 256 * sizeof(long long), cudaMemcpyDeviceToHost);
 }

@@ -313,18 +313,14 @@ __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_consta
           flag[0] = (prev == hi - lo) ? 1 : 0;
           flag[1] = lo;
           flag[2] = hi;
+          flag[3] = ((int)((int64_t)lo * p.units / grid) / KT == nt) ? 0 : 1;
         }
         named_bar_sync(1, kTc2Groups * 128);
         if (flag[0]) {
           __threadfence();
           const int lo = flag[1], hi = flag[2];
           for (int m = g; m < p.M; m += kTc2Groups) {
-            float sum = 0.f;
-            for (int qq = lo; qq <= hi; ++qq) {
-              const int q_first = (int)((int64_t)qq * p.units / grid) / KT;
-              const int qslot = (nt == q_first) ? 0 : 1;
-              sum += __ldcg(p.partial + ((int64_t)(qq * 2 + qslot) * NB + m) * kBN + n);
-            }
+            const float sum = streamk_sum(p.partial, lo, hi, flag[3], (int64_t)NB * kBN, (int64_t)m * kBN + n);
             p.Y[(int64_t)m * p.ldy + col] = __float2half_rn(sum);
           }
           if (threadIdx.x == 64) p.sem[nt] = 0;

@@ -216,6 +216,7 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   } else {
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (threadIdx.x == 64) tcd_stamp(p, 11);
     if constexpr (kInt) {
       // sum_k A[m, k] of every 128-k tile (zero-point term), 4 (tile, row) pairs per warp in flight
       float* sums_w = reinterpret_cast<float*>(smem + p.sums_off);
@@ -491,18 +492,14 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
           flag[0] = (prev == hi - lo) ? 1 : 0;
           flag[1] = lo;
           flag[2] = hi;
+          flag[3] = ((int)((int64_t)lo * p.units / grid) / KT == nt) ? 0 : 1;
         }
         named_bar_sync(1, NG * 128);
         if (flag[0]) {
           __threadfence();
           const int lo = flag[1], hi = flag[2];
           for (int m = g; m < p.M; m += NG) {
-            float sum = 0.f;
-            for (int qq = lo; qq <= hi; ++qq) {
-              const int q_first = (int)((int64_t)qq * p.units / grid) / KT;
-              const int qslot = (nt == q_first) ? 0 : 1;
-              sum += __ldcg(p.partial + ((int64_t)(qq * 2 + qslot) * kTcdNB + m) * kBN + n);
-            }
+            const float sum = streamk_sum(p.partial, lo, hi, flag[3], (int64_t)kTcdNB * kBN, (int64_t)m * kBN + n);
             p.Y[(int64_t)m * p.ldy + col] = __float2half_rn(sum);
           }
           if (threadIdx.x == 128) p.sem[nt] = 0;
@@ -539,7 +536,7 @@ tl_status launch_tcd_mt(const TcdParams& p, const CUtensorMap* tmap, int grid, u
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = (p.dbg & 128) ? 0 : 1;  // TL_TCD_DBG=128: plain stream order (A/B of the PDL overlap)
   cudaError_t e = cudaLaunchKernelEx(&cfg, tcd_kernel<F, MT>, *tmap, p);
   if (e != cudaSuccess) return fail(TL_ECUDA, "tcd_kernel launch: %s", cudaGetErrorString(e));
   return check_launch("tcd_kernel");
