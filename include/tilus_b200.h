@@ -71,10 +71,13 @@ typedef enum {
 /* Which kernel family tl_matmul uses (CUDA cores for few tokens,
  * tensor cores for more; the crossover is re-measured on B200):
  *   TL_PATH_GEMV  CUDA-core GEMV / skinny GEMM (FHFMA, fp32 accumulation), any M (16 rows per launch)
- *   TL_PATH_TC    tcgen05 GEMM, dequantized weight tile in shared memory, scale applied in fp16 (any M)
- *   TL_PATH_TCS   tcgen05 decode variant for M <= 16 and group >= 128: weight tile in tensor
- *                 memory, scale / zero point applied per tile in fp32 (falls back to TL_PATH_TC
- *                 when the shape is outside that range) */
+ *   TL_PATH_TC    tcgen05 GEMM, dequantized W^T in tensor memory, batch as MMA-N (any M)
+ *   TL_PATH_TCS   tcgen05 decode kernel for M <= 16 and group a multiple of 128: W^T unpacked into
+ *                 tensor memory as exact fp16 values, scale / zero point applied per tile in fp32,
+ *                 launched with programmatic dependent launch (its weight stream may start before
+ *                 the previous kernel in the stream ends; A, Y and the workspace are touched only
+ *                 after that kernel completed).  Falls back to TL_PATH_TC outside that range.
+ * TL_PATH_AUTO: TL_PATH_TCS when eligible, else TL_PATH_GEMV for M <= 1, else TL_PATH_TC. */
 typedef enum { TL_PATH_AUTO = 0, TL_PATH_GEMV = 1, TL_PATH_TC = 2, TL_PATH_TCS = 3 } tl_path;
 
 /* ---- sizes --------------------------------------------------------------- */

@@ -218,33 +218,28 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (threadIdx.x == 64) tcd_stamp(p, 11);
     if constexpr (kInt) {
-      // sum_k A[m, k] of every 128-k tile (zero-point term), 4 (tile, row) pairs per warp in flight
+      // sum_k A[m, k] of every 128-k tile (zero-point term): one thread per (tile, row), its 256 B
+      // loaded with 16 independent 16-byte loads (one L2 round trip), summed in fp32 in k order
       float* sums_w = reinterpret_cast<float*>(smem + p.sums_off);
       const int n_pairs = KT * p.M;
-      for (int i0 = (warp - 1) * 4; i0 < n_pairs; i0 += (kTcdThreads / 32 - 1) * 4) {
-        uint2 v[4];
+      for (int i = threadIdx.x - 32; i < n_pairs; i += kTcdThreads - 32) {
+        const int kt = i / p.M, m = i - (i / p.M) * p.M;
+        const uint4* src = reinterpret_cast<const uint4*>(p.A + m * p.lda + (int64_t)kt * kBK);
+        uint4 v[16];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int i = min(i0 + j, n_pairs - 1);
-          const int kt = i / p.M, m = i - (i / p.M) * p.M;
-          v[j] = __ldg(reinterpret_cast<const uint2*>(p.A + m * p.lda + (int64_t)kt * kBK) + lane);
-        }
-        float sm[4];
+        for (int j = 0; j < 16; ++j) v[j] = __ldg(src + j);
+        float acc = 0.f;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 f0 = __half22float2(u32_as_h2(v[j].x)), f1 = __half22float2(u32_as_h2(v[j].y));
-          sm[j] = (f0.x + f0.y) + (f1.x + f1.y);
-        }
+        for (int j = 0; j < 16; ++j) {
+          const uint32_t w4[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
 #pragma unroll
-        for (int d = 16; d >= 1; d >>= 1)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) sm[j] += __shfl_xor_sync(0xffffffffu, sm[j], d);
-        if (lane == 0)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int i = i0 + j;
-            if (i < n_pairs) sums_w[(i / p.M) * MT + (i - (i / p.M) * p.M)] = sm[j];
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __half22float2(u32_as_h2(w4[e]));
+            acc += f.x;
+            acc += f.y;
           }
+        }
+        sums_w[kt * MT + m] = acc;
       }
     }
     named_bar_sync(2, kTcdThreads - 32);  // sums visible to the dequant groups
