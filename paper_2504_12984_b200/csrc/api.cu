@@ -34,8 +34,9 @@ static int choose_path(tl_wtype w, int64_t M, int32_t G) {
   if (forced == TL_PATH_GEMV || forced == TL_PATH_TC || forced == TL_PATH_TCS) return forced;
   if (!tc_available()) return TL_PATH_GEMV;
   (void)w;
-  // measured on B200: the CUDA-core path is fastest at M = 1, the
-  // tensor-memory decode variant for 2 <= M <= 16 (group >= 128), the smem variant otherwise
+  // measured on B200: the tensor-core decode kernel (tcd) for M <= 16 with a group
+  // that is a multiple of 128 (it beats the CUDA-core GEMV from M = 1), the CUDA-core GEMV for the
+  // remaining decode shapes (G = 32, 64), the tcgen05 GEMM above M = 16
   if (tcs_eligible(M, G)) return TL_PATH_TCS;
   if (M <= 1) return TL_PATH_GEMV;
   return TL_PATH_TC;
