@@ -478,12 +478,15 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
         else __stcg(part + (int64_t)m * kBN + n, v);
       }
       if (!complete) {
-        __threadfence();
+        // publish: the CTA barrier orders every thread's partial store before thread 128's
+        // gpu-scope acq_rel increment (release for ours, acquire of the other CTAs' partials when
+        // we are the last to arrive); no per-thread fences
         named_bar_sync(1, NG * 128);
         if (threadIdx.x == 128) {
           const int lo = (int)((((int64_t)ua + 1) * grid - 1) / p.units);
           const int hi = (int)((((int64_t)ub) * grid - 1) / p.units);
-          const int prev = atomicAdd(&p.sem[nt], 1);
+          int prev;
+          asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(&p.sem[nt]) : "memory");
           flag[0] = (prev == hi - lo) ? 1 : 0;
           flag[1] = lo;
           flag[2] = hi;
@@ -491,7 +494,6 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
         }
         named_bar_sync(1, NG * 128);
         if (flag[0]) {
-          __threadfence();
           const int lo = flag[1], hi = flag[2];
           for (int m = g; m < p.M; m += NG) {
             const float sum = streamk_sum(p.partial, lo, hi, flag[3], (int64_t)kTcdNB * kBN, (int64_t)m * kBN + n);
