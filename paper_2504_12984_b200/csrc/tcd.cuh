@@ -218,28 +218,32 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (threadIdx.x == 64) tcd_stamp(p, 11);
     if constexpr (kInt) {
-      // sum_k A[m, k] of every 128-k tile (zero-point term): one thread per (tile, row), its 256 B
-      // loaded with 16 independent 16-byte loads (one L2 round trip), summed in fp32 in k order
+      // sum_k A[m, k] of the 128-k tiles this CTA touches (zero-point term): one thread per
+      // (tile, row), its 256 B loaded with 16 independent 16-byte loads (one L2 round trip) and
+      // summed in fp32 by four independent chains
       float* sums_w = reinterpret_cast<float*>(smem + p.sums_off);
-      const int n_pairs = KT * p.M;
+      const int nk = min(KT, T), kt0 = u0 - (u0 / KT) * KT;
+      const int n_pairs = (p.dbg & 256) ? 0 : nk * p.M;
       for (int i = threadIdx.x - 32; i < n_pairs; i += kTcdThreads - 32) {
-        const int kt = i / p.M, m = i - (i / p.M) * p.M;
+        int kt = kt0 + i / p.M;
+        if (kt >= KT) kt -= KT;
+        const int m = i - (i / p.M) * p.M;
         const uint4* src = reinterpret_cast<const uint4*>(p.A + m * p.lda + (int64_t)kt * kBK);
         uint4 v[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = __ldg(src + j);
-        float acc = 0.f;
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const uint32_t w4[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const float2 f = __half22float2(u32_as_h2(w4[e]));
-            acc += f.x;
-            acc += f.y;
+            acc[e] += f.x;
+            acc[e] += f.y;
           }
         }
-        sums_w[kt * MT + m] = acc;
+        sums_w[kt * MT + m] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
       }
     }
     named_bar_sync(2, kTcdThreads - 32);  // sums visible to the dequant groups
