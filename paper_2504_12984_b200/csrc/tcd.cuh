@@ -62,8 +62,15 @@ struct TcdParams {
 };
 
 constexpr int kTcdNG = 4;                       // dequant groups
-constexpr int kTcdNW = 5;                       // W^T TMEM slots (64 columns each), slot = tile % 5
-constexpr int kTcdNACC = 12;                    // accumulator slots (16 TMEM columns each): 5*64 + 12*16 = 512
+#ifndef TCD_NW
+#define TCD_NW 5
+#endif
+constexpr int kTcdNW = TCD_NW;                  // W^T TMEM slots (64 columns each), slot = tile % NW
+constexpr int kTcdNACC = (512 - 64 * kTcdNW) / 16; // accumulator slots (16 TMEM columns each): NW*64 + NACC*16 = 512
+// fixups lag this many group iterations; the accumulator of tile t - NACC must be read by its group
+// before that group arrives for tile t: 4*lag < NACC
+constexpr int kTcdLag = kTcdNACC / 4 - 1;
+static_assert(kTcdNACC % 4 == 0 && kTcdLag >= 1 && kTcdLag <= 2, "TMEM split");
 constexpr int kTcdThreads = 128 + kTcdNG * 128;
 constexpr int kTcdNB = 16;                      // MMA N (batch rows, zero-padded)
 constexpr uint32_t kTcdOpBytes = kTcdNB * 256;  // 16 rows x 128 k fp16, two 64-k SW128 blocks
@@ -447,9 +454,13 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
           wsl -= kTcdNW;
           ++lapw;
         }
-        if (tp2 >= 0) fixup(tp2, c1p2);
-        tp2 = tp1;
-        c1p2 = c1p1;
+        if constexpr (kTcdLag == 2) {
+          if (tp2 >= 0) fixup(tp2, c1p2);
+          tp2 = tp1;
+          c1p2 = c1p1;
+        } else {
+          if (tp1 >= 0) fixup(tp1, c1p1);
+        }
         tcd_istamp(p, dw, lane, kk, 6);
         tp1 = t;
         c1p1 = sc * c1mul;
