@@ -58,7 +58,8 @@ struct TcdParams {
   float* partial;  // [grid][2][16][128] fp32
   int* sem;
   long long* trace;  // optional [grid][16] %globaltimer stamps (TL_TRACE)
-  int dbg;  // debug knobs (TL_TCD_DBG): 1 skip MMAs, 2 skip prep arithmetic, 4 skip unpack/STTM
+  int dbg;  // experiment knobs (TL_TCD_DBG; device-side ones only with -DTCD_TRACE): 1 skip MMAs,
+            // 4 skip unpack/STTM, 8 skip scale/zero copies, 128 no PDL (host), 256 skip activation sums
 };
 
 constexpr int kTcdNG = 4;                       // dequant groups
@@ -134,17 +135,28 @@ __device__ __forceinline__ void tcd_load_words(uint32_t wtile, int n, uint32_t* 
   }
 }
 
+// Pipeline tracing (tools/trace_tcd.py, tools/trace_pdl.py): compiled in only with -DTCD_TRACE,
+// so the production kernel carries no trace branches.
+#ifdef TCD_TRACE
+#define TCD_TRACE_ON 1
+#else
+#define TCD_TRACE_ON 0
+#endif
 __device__ __forceinline__ void tcd_stamp(const TcdParams& p, int i) {
-  if (p.trace != nullptr) {
+  if (TCD_TRACE_ON && p.trace != nullptr) {
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     p.trace[blockIdx.x * 16 + i] = t;
   }
 }
+__device__ __forceinline__ void tcd_tstamp(const TcdParams& p, int idx) {  // clock64 of CTA 0
+  if (TCD_TRACE_ON && p.trace != nullptr && blockIdx.x == 0) p.trace[idx] = clock64();
+}
 
-// per-iteration clock64 stamps of CTA 0, group 0, warp 0, lane 0 (TL_TRACE): [iter][8] at 2400
+// per-iteration clock64 stamps of CTA 0, group 0, warp 0, lane 0: [iter][8] at 2400
 __device__ __forceinline__ void tcd_istamp(const TcdParams& p, int dw, int lane, uint32_t kk, int i) {
-  if (p.trace != nullptr && blockIdx.x == 0 && dw == 0 && lane == 0 && kk < 40) p.trace[2400 + kk * 8 + i] = clock64();
+  if (TCD_TRACE_ON && p.trace != nullptr && blockIdx.x == 0 && dw == 0 && lane == 0 && kk < 40)
+    p.trace[2400 + kk * 8 + i] = clock64();
 }
 
 template <class F, int MT>
@@ -186,7 +198,7 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
 
   if (threadIdx.x == 0) {
     tcd_stamp(p, 0);
-    if (p.trace) p.trace[blockIdx.x * 16 + 10] = T;
+    if (TCD_TRACE_ON && p.trace) p.trace[blockIdx.x * 16 + 10] = T;
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full_tma[s], 1);
       mbar_init(&empty_tma[s], 4);
@@ -230,7 +242,7 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
       // summed in fp32 by four independent chains
       float* sums_w = reinterpret_cast<float*>(smem + p.sums_off);
       const int nk = min(KT, T), kt0 = u0 - (u0 / KT) * KT;
-      const int n_pairs = (p.dbg & 256) ? 0 : nk * p.M;
+      const int n_pairs = (TCD_TRACE_ON && (p.dbg & 256)) ? 0 : nk * p.M;
       for (int i = threadIdx.x - 32; i < n_pairs; i += kTcdThreads - 32) {
         int kt = kt0 + i / p.M;
         if (kt >= KT) kt -= KT;
@@ -268,7 +280,7 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
       const uint64_t pol_last = policy_evict_last();
       int nt = u0 / KT, kt = u0 - (u0 / KT) * KT;
       if (warp == 0) {
-        const bool side = !(p.dbg & 8);
+        const bool side = !(TCD_TRACE_ON && (p.dbg & 8));
         const uint32_t bytes = WB + (side ? 256u + (has_zeros ? 256u : 0u) : 0u);
         const uint32_t bar0 = smem_u32(full_tma);
         const uint8_t* src = p.wt + (int64_t)u0 * WB;
@@ -278,7 +290,7 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
         uint32_t ph = 0;
         for (int t = 0; t < T; ++t) {
           if (t >= NS) mbar_wait(&empty_tma[s], ph ^ 1);
-          if (p.trace && blockIdx.x == 0 && t < 64) p.trace[2720 + t] = clock64();
+          if (t < 64) tcd_tstamp(p, 2720 + t);
           const uint32_t st = st_u + s * SB, bar = bar0 + 8 * s;
           mbar_arrive_expect_tx_u32(bar, bytes);
           tma_bulk_g2s_cta(st + p.w_off, src, WB, bar, pol_first);
@@ -333,19 +345,19 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
       uint32_t kk = 0, ka = 0;  // t / NW, t / NACC
       for (int t = 0; t < T; ++t) {
         mbar_wait(&full_w[g], kk & 1);
-        if (p.trace && blockIdx.x == 0 && t < 64) p.trace[2976 + 3 * t] = clock64();
-        if (p.trace && blockIdx.x == 0 && t < 64) p.trace[2977 + 3 * t] = clock64();
+        if (t < 64) tcd_tstamp(p, 2976 + 3 * t);
+        if (t < 64) tcd_tstamp(p, 2977 + 3 * t);
         tc_fence_after();
         const uint64_t bd = tcd_sw128_desc(op_u + o * kTcdOpBytes);
         const uint32_t d = tmem + kTcdAccCol + a * kTcdNB;
         const uint32_t aw = tmem + g * 64;
-        if (!(p.dbg & 1))
+        if (!(TCD_TRACE_ON && (p.dbg & 1)))
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           tcd_mma_ts(d, aw + j * 8, bd + (uint64_t)((j >> 2) * (kTcdNB * 128 / 16) + (j & 3) * 2), idesc,
                      j > 0 ? 1u : 0u);
         tc_commit(&full_acc[a]);  // "MMA(t) complete": frees W^T slot t%NW, operand slot t%NOP, fills acc t%NACC
-        if (p.trace && blockIdx.x == 0 && t < 64) p.trace[2978 + 3 * t] = clock64();
+        if (t < 64) tcd_tstamp(p, 2978 + 3 * t);
         if (t == T - 1) tcd_stamp(p, 8);
         if (++o == kTcdNOP) o = 0;
         if (++g == kTcdNW) {
@@ -432,7 +444,7 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
         if (t >= kTcdNW) mbar_wait(&full_acc[(t - kTcdNW) % NACC], (uint32_t)((t - kTcdNW) / NACC) & 1);
         const uint32_t tslot = tmem + lane_off + wsl * 64;
         tcd_istamp(p, dw, lane, kk, 3);
-        if (!(p.dbg & 4)) static_for<0, 4>([&](auto CC) {
+        if (!(TCD_TRACE_ON && (p.dbg & 4))) static_for<0, 4>([&](auto CC) {
           constexpr int c = decltype(CC)::value;
           uint32_t r[16];
           static_for<0, 16>([&](auto II) {

@@ -1,4 +1,4 @@
-"""Per-CTA %globaltimer stamps of one tcd launch (TL_TRACE=1): where a launch's time goes."""
+"""Per-CTA %globaltimer stamps of one tcd launch (TL_TRACE=1; the library built with -DTCD_TRACE)."""
 import ctypes, os, sys
 os.environ["TL_TRACE"] = "1"
 sys.path.insert(0, ".")
