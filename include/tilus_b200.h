@@ -74,9 +74,12 @@ typedef enum {
  *   TL_PATH_TC    tcgen05 GEMM, dequantized W^T in tensor memory, batch as MMA-N (any M)
  *   TL_PATH_TCS   tcgen05 decode kernel for M <= 16 and group a multiple of 128: W^T unpacked into
  *                 tensor memory as exact fp16 values, scale / zero point applied per tile in fp32,
- *                 launched with programmatic dependent launch (its weight stream may start before
- *                 the previous kernel in the stream ends; A, Y and the workspace are touched only
- *                 after that kernel completed).  Falls back to TL_PATH_TC outside that range.
+ *                 launched with programmatic dependent launch: when the previous kernel in the stream
+ *                 is itself such a launch (it signals early and never writes weights, scales or
+ *                 zeros), this launch's weight stream starts before it ends; A, Y and the workspace
+ *                 are touched only after it completed.  Any other preceding kernel (e.g. the one that
+ *                 wrote the weights) completes first, as in plain stream order.  Falls back to
+ *                 TL_PATH_TC outside that range.
  * TL_PATH_AUTO: TL_PATH_TCS when eligible, else TL_PATH_GEMV for M <= 1, else TL_PATH_TC. */
 typedef enum { TL_PATH_AUTO = 0, TL_PATH_GEMV = 1, TL_PATH_TC = 2, TL_PATH_TCS = 3 } tl_path;
 
