@@ -78,7 +78,9 @@ def test_bad_arguments_rejected_before_any_launch(lib):
     # M == 0 is a no-op
     st = lib._lib._tl_matmul(w, 0, 128, 128, 128, 16, 128, 16, 16, None, 16, 128, 16, 1 << 24, None)
     assert st == 0
-    assert "workspace" in lib._lib._tl_last_error().decode() or True
+    st = lib._lib._tl_matmul(w, 1, 128, 128, 128, 16, 128, 16, 16, None, 16, 128, 16, 64, None)
+    assert lib._lib._tl_status_str(st).decode() == "TL_EWORKSPACE"
+    assert "workspace" in lib._lib._tl_last_error().decode()
     del torch
 
 

@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 import workloads as wl
-from helpers import make_problem, prepare_weights, run_matmul, to_dev
+from helpers import check_oracle, make_problem, prepare_weights, run_matmul, to_dev
 from oracle import all_kernel_formats, dequant, matmul_cols_fp64, matmul_fp64, parse_wtype, tolerance_check
 
 pytestmark = pytest.mark.gpu
@@ -23,12 +23,7 @@ def env():
     return P, torch
 
 
-def _check(fmt, A, codes, scales, zeros, G, Y):
-    w = dequant(parse_wtype(fmt), codes, scales, zeros, G)
-    Y64 = matmul_fp64(A, w)
-    r = tolerance_check(Y, Y64, A, w)
-    assert r["ok"], r
-    return r
+_check = check_oracle
 
 
 @pytest.mark.parametrize("path", list(PATHS))
@@ -62,18 +57,16 @@ def test_matmul_exact_integer_instance_bit_exact(env, fmt, path):
 
 @pytest.mark.parametrize("path", list(PATHS))
 def test_matmul_grid_sweep_stream_k(env, path):
-    """Every stream-K partition (1 CTA ... one CTA per tile) gives the same bits."""
+    """Every stream-K partition (1 CTA ... one CTA per tile) is within O7 of the oracle.  Different
+    partitions sum the K range in different orders, so they agree within tolerance, not in bits
+    (run-to-run identity of ONE partition is test_matmul_deterministic_and_fully_written)."""
     P, torch = env
     fmt, M, K, N, G = "u4", 2, 1024, 512, 128
     A, codes, s, z = make_problem(fmt, M, K, N, G)
     w, _, wt = prepare_weights(P, torch, fmt, K, N, codes)
-    ref = None
     for grid in [1, 3, 5, 7, 8, 13, 31, 32]:
         Y, _, _ = run_matmul(P, torch, fmt, A, codes, s, z, G, path=PATHS[path], splits=grid, wt=wt)
         _check(fmt, A, codes, s, z, G, Y)
-        if ref is None:
-            ref = Y
-    # different partitions sum in different orders: equal within tolerance, not bits
 
 
 @pytest.mark.parametrize("path", list(PATHS))

@@ -208,3 +208,64 @@ def test_exact_instance_is_exact():
     for k in reversed(range(K)):
         rev += A[:, k:k + 1].astype(np.float32) * w[k:k + 1].astype(np.float32)
     assert np.array_equal(fwd, y64) and np.array_equal(rev, y64)
+
+
+def _elementwise_case():
+    """A problem where rel-Frobenius stays far below 1e-3 while one element misses by more than
+    1e-2 * ||A_m|| * ||w_n||: only O7's element-wise clause (north star) can reject it."""
+    rng = np.random.default_rng(7)
+    M, K, N = 64, 256, 4096
+    A = rng.standard_normal((M, K)).astype(np.float16)
+    w = rng.standard_normal((K, N)) * 0.02
+    Y64 = matmul_fp64(A, w)
+    bound = 1e-2 * np.linalg.norm(A.astype(np.float64), axis=1)[:, None] * np.linalg.norm(w, axis=0)[None, :]
+    return A, w, Y64, bound
+
+
+def test_tolerance_elementwise_clause_rejects_single_outlier():
+    A, w, Y64, bound = _elementwise_case()
+    Y = Y64.astype(np.float16)
+    m, n = 37, 2049
+    Y[m, n] = np.float16(Y64[m, n] + 1.5 * bound[m, n])
+    d = Y.astype(np.float64) - Y64
+    rel = np.linalg.norm(d) / np.linalg.norm(Y64)
+    assert rel <= 1e-3                              # the Frobenius clause alone would accept it
+    assert abs(d[m, n]) > bound[m, n]               # ... the element-wise clause must not
+    r = tolerance_check(Y, Y64, A, w)
+    assert not r["ok"] and r["rel_fro"] <= 1e-3
+    # the clause is per (row, column): the same absolute error on an element whose row norm is
+    # 4x larger is inside its own bound
+    A2 = A.copy()
+    A2[m] *= 4
+    Y64b = matmul_fp64(A2, w)
+    Yb = Y64b.astype(np.float16)
+    Yb[m, n] = np.float16(Y64b[m, n] + 1.5 * bound[m, n])
+    assert tolerance_check(Yb, Y64b, A2, w)["ok"]
+
+
+def test_tolerance_elementwise_clause_uses_row_and_column_norms():
+    """Mis-axing the bound (column norm of A, row norm of w) would change which element passes:
+    a column of w 10x smaller than the rest tightens only that column's bound."""
+    A, w, Y64, _ = _elementwise_case()
+    w = w.copy()
+    w[:, 5] *= 0.1
+    Y64 = matmul_fp64(A, w)
+    bcol = 1e-2 * np.linalg.norm(A[0].astype(np.float64)) * np.linalg.norm(w[:, 5])
+    Y = Y64.astype(np.float16)
+    Y[0, 5] = np.float16(Y64[0, 5] + 2.0 * bcol)       # outside column 5's (small) bound
+    assert not tolerance_check(Y, Y64, A, w)["ok"]
+    Y = Y64.astype(np.float16)
+    Y[0, 6] = np.float16(Y64[0, 6] + 2.0 * bcol)       # same error, inside column 6's bound
+    assert tolerance_check(Y, Y64, A, w)["ok"]
+
+
+def test_tolerance_max_abs_ratio_is_the_guard_statistic():
+    """max_abs_ratio = max |Y - Y64| / (||A_m|| ||w_n||): the statistic the GPU tests also hold to
+    the 1e-3 internal regression guard (observed ~1.5e-5 for fp16 output)."""
+    A, w, Y64, bound = _elementwise_case()
+    Y = Y64.astype(np.float16)
+    r = tolerance_check(Y, Y64, A, w)
+    assert r["ok"] and r["max_abs_ratio"] < 1e-4
+    Y[3, 3] = np.float16(Y64[3, 3] + 0.5 * bound[3, 3])   # 5e-3 of the norm product: inside O7
+    r = tolerance_check(Y, Y64, A, w)
+    assert r["ok"] and 4e-3 < r["max_abs_ratio"] < 6e-3   # ... but 5x over the 1e-3 guard
