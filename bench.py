@@ -188,6 +188,9 @@ def run_ours(args):
     G = 128
     M = args.M
     layers = {k: wl.LLAMA33_70B[k] for k in args.layers}
+    # resident model weights, prepared once before the timed region: the decode kernel's weight
+    # stream may overlap the previous launch's tail (programmatic dependent launch, header)
+    FLAGS = P.TL_FLAG_STATIC_WEIGHTS
 
     # ---- one-time weight preparation (untimed) ----
     probs = []
@@ -217,7 +220,7 @@ def run_ours(args):
         for i, p in enumerate(probs):
             if events is not None:
                 events[i][0].record(stream)
-            P.tl_matmul(p["w"], m, p["N"], p["K"], G, p["A"], p["wt"], p["s"], p["z"], p["Y"], ws)
+            P.tl_matmul_ex(p["w"], m, p["N"], p["K"], G, p["A"], p["wt"], p["s"], p["z"], p["Y"], ws, flags=FLAGS)
             if events is not None:
                 events[i][1].record(stream)
             if args.gather:
@@ -259,7 +262,8 @@ def run_ours(args):
             with torch.cuda.graph(g2):
                 evs[0].record()
                 for i, p in enumerate(probs):
-                    P.tl_matmul(p["w"], m, p["N"], p["K"], G, p["A"], p["wt"], p["s"], p["z"], p["Y"], ws)
+                    P.tl_matmul_ex(p["w"], m, p["N"], p["K"], G, p["A"], p["wt"], p["s"], p["z"], p["Y"], ws,
+                                   flags=FLAGS)
                     evs[i + 1].record()
             g2.replay()
             torch.cuda.synchronize()
@@ -347,7 +351,8 @@ def run_ours(args):
 
         def step_e2e():
             for p, (Ah, Yh) in zip(probs, host):
-                P.tl_matmul_hostio(p["w"], M, p["N"], p["K"], G, Ah, p["A"], p["wt"], p["s"], p["z"], p["Y"], Yh, ws)
+                P.tl_matmul_hostio(p["w"], M, p["N"], p["K"], G, Ah, p["A"], p["wt"], p["s"], p["z"], p["Y"], Yh, ws,
+                                   flags=FLAGS)
 
         for _ in range(args.warmup):
             step_e2e()

@@ -17,7 +17,9 @@
  * call.  The transformed layout is opaque and versioned (tl_format_version).
  *
  * Conventions (all functions):
- *   - extern "C", thread-safe, never throw, never synchronise the host.
+ *   - extern "C", never throw, never synchronise the host.  Thread-safe: per-device kernel
+ *     attributes are set once per (kernel, device) under a lock; the error message is
+ *     thread-local.
  *   - Every pointer argument is a DEVICE pointer unless its name ends in _host.
  *   - The caller owns every buffer (including the workspace); the library never
  *     allocates on the hot path, so calls are CUDA-graph capturable.
@@ -53,7 +55,10 @@ typedef struct {
   uint8_t man_bits;
 } tl_wtype;
 
-typedef enum { TL_ACT_F16 = 0 } tl_atype; /* activations, scales and Y are fp16 */
+/* Activation type: the dtype of A, of the scales and of Y ("A ... float16";
+ * PAPER.md:527 "we also support bfloat16").  TL_ACT_BF16 is reserved in this build: calls that
+ * pass it return TL_EUNSUPPORTED. */
+typedef enum { TL_ACT_F16 = 0, TL_ACT_BF16 = 1 } tl_atype;
 
 typedef enum {
   TL_OK = 0,
@@ -68,20 +73,28 @@ typedef enum {
   TL_ENULL = 9          /* a required pointer is NULL                           */
 } tl_status;
 
-/* Which kernel family tl_matmul uses (CUDA cores for few tokens,
- * tensor cores for more; the crossover is re-measured on B200):
+/* Which kernel family tl_matmul uses (CUDA cores for few tokens, tensor cores for
+ * more; on B200 the choice is re-measured):
  *   TL_PATH_GEMV  CUDA-core GEMV / skinny GEMM (FHFMA, fp32 accumulation), any M (16 rows per launch)
  *   TL_PATH_TC    tcgen05 GEMM, dequantized W^T in tensor memory, batch as MMA-N (any M)
- *   TL_PATH_TCS   tcgen05 decode kernel for M <= 16 and group a multiple of 128: W^T unpacked into
+ *   TL_PATH_TCD   tcgen05 decode kernel for M <= 16 and group a multiple of 128: W^T unpacked into
  *                 tensor memory as exact fp16 values, scale / zero point applied per tile in fp32,
- *                 launched with programmatic dependent launch: when the previous kernel in the stream
- *                 is itself such a launch (it signals early and never writes weights, scales or
- *                 zeros), this launch's weight stream starts before it ends; A, Y and the workspace
- *                 are touched only after it completed.  Any other preceding kernel (e.g. the one that
- *                 wrote the weights) completes first, as in plain stream order.  Falls back to
- *                 TL_PATH_TC outside that range.
- * TL_PATH_AUTO: TL_PATH_TCS when eligible, else TL_PATH_GEMV for M <= 1, else TL_PATH_TC. */
-typedef enum { TL_PATH_AUTO = 0, TL_PATH_GEMV = 1, TL_PATH_TC = 2, TL_PATH_TCS = 3 } tl_path;
+ *                 launched with programmatic dependent launch (see TL_FLAG_STATIC_WEIGHTS).  Falls
+ *                 back to TL_PATH_TC outside that range.
+ * TL_PATH_AUTO: the measured dispatch rule. */
+typedef enum { TL_PATH_AUTO = 0, TL_PATH_GEMV = 1, TL_PATH_TC = 2, TL_PATH_TCD = 3 } tl_path;
+
+/* tl_matmul_ex / tl_matmul_hostio flags.
+ *   TL_FLAG_STATIC_WEIGHTS  w_t, scales and zeros are not written by any kernel that may still be
+ *     running on `stream` when this call is enqueued (e.g. resident model weights prepared long
+ *     before).  The decode kernel (TL_PATH_TCD) is launched with programmatic dependent launch: its
+ *     CTAs may start while the previous kernel in the stream is finishing.  With this flag its
+ *     weight / scale / zero stream starts at once, overlapping that tail; A, Y and the workspace
+ *     are touched only after griddepcontrol.wait (the previous grid completed, its writes
+ *     visible).  Without the flag every read waits, so a transform or scale-producing kernel may
+ *     directly precede the matmul: PTX guarantees the visibility of a prerequisite grid's writes
+ *     only after griddepcontrol.wait. */
+#define TL_FLAG_STATIC_WEIGHTS 1u
 
 /* ---- sizes --------------------------------------------------------------- */
 
@@ -121,37 +134,43 @@ tl_status tl_untransform_weights(tl_wtype w, int64_t K, int64_t N, const void* w
 
 /* ---- the hot path ------------------------------------------------------------ */
 
-/* Workspace bytes tl_matmul needs for this problem (split-K partials and tile
- * semaphores).  The workspace must be ZERO-FILLED once when allocated; the
- * kernels leave every semaphore at zero again when they finish, so it can be
- * reused by any later call on the same stream without clearing. */
-size_t tl_matmul_workspace_bytes(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t group);
+/* Workspace bytes tl_matmul needs for this problem (split-K partials and tile semaphores): the
+ * global workspace of the paper's runtime, which kernels request via AllocateGlobal
+ * (PAPER.md:439-440), here owned by the caller so calls stay graph-capturable.
+ * The workspace must be ZERO-FILLED once when allocated; the kernels leave every semaphore at zero
+ * again when they finish, so it can be reused by any later call on the same stream without
+ * clearing.  Returns 0 for an unsupported activation type. */
+size_t tl_matmul_workspace_bytes(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group);
 
-/* Y[M,N] (row stride ldy elements, fp16) = A[M,K] (row stride lda elements, fp16)
- * x dequant(w_t).  scales: [K/G, N] fp16 row-major.  zeros: [K/G, N] fp16 with
- * integer values, uint formats only, or NULL (z = 0).  Enqueued on `stream`. */
-tl_status tl_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t group, const void* A,
+/* Y[M,N] (row stride ldy elements) = A[M,K] (row stride lda elements) x dequant(w_t): the paper's
+ * C = A x B with fp32 accumulation cast to the activation type.
+ * A, scales and Y have type `a`.  scales: [K/G, N] row-major.  zeros: [K/G, N] with integer
+ * values, uint formats only, or NULL (z = 0).  Enqueued on `stream`; no flags: every read is
+ * ordered after the previous kernel in the stream. */
+tl_status tl_matmul(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group, const void* A,
                     int64_t lda, const void* w_t, const void* scales, const void* zeros, void* Y,
                     int64_t ldy, void* workspace, size_t workspace_bytes, void* stream);
 
-/* As tl_matmul with an explicit kernel family and split-K factor (0 = auto);
- * used by the dispatch sweep and the tests. */
-tl_status tl_matmul_ex(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t group, const void* A,
-                       int64_t lda, const void* w_t, const void* scales, const void* zeros,
-                       void* Y, int64_t ldy, void* workspace, size_t workspace_bytes,
-                       int32_t path, int32_t splits, void* stream);
+/* As tl_matmul with an explicit kernel family (tl_path), split-K grid (0 = auto; requests above
+ * the CTA count the workspace is sized for are clamped to it) and flags (TL_FLAG_*); used by the
+ * bench, the dispatch sweep and the tests. */
+tl_status tl_matmul_ex(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group,
+                       const void* A, int64_t lda, const void* w_t, const void* scales,
+                       const void* zeros, void* Y, int64_t ldy, void* workspace, size_t workspace_bytes,
+                       int32_t path, int32_t splits, uint32_t flags, void* stream);
 
 /* End-to-end variant for host buffers: copies A_host [M,K] (pinned recommended)
  * into the device staging buffer A_dev, runs tl_matmul into Y_dev and copies
  * Y_dev back into Y_host [M,N], all on `stream` (no host sync).  Weights,
- * scales and zeros stay resident on the device. */
-tl_status tl_matmul_hostio(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t group,
+ * scales and zeros stay resident on the device (flags as tl_matmul_ex). */
+tl_status tl_matmul_hostio(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group,
                            const void* A_host, void* A_dev, const void* w_t, const void* scales,
                            const void* zeros, void* Y_dev, void* Y_host, void* workspace,
-                           size_t workspace_bytes, void* stream);
+                           size_t workspace_bytes, uint32_t flags, void* stream);
 
-/* Which family / split tl_matmul would pick for this shape (for the bench). */
-tl_status tl_matmul_plan(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t group,
+/* Which family (tl_path) and split-K grid tl_matmul would use for this problem on the current
+ * device (for the bench and the dispatch sweep); *splits_out = 0 means one CTA per SM. */
+tl_status tl_matmul_plan(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group,
                          int32_t* path_out, int32_t* splits_out);
 
 /* Test hook: out[K,N] fp32 = (value(q) - z) * s, computed exactly in fp32 from

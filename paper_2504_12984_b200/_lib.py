@@ -53,7 +53,9 @@ def wtype(name: str) -> tl_wtype:
     return tl_wtype(2, int(m.group(3)), int(m.group(4)), int(m.group(5)))
 
 
-TL_PATH_AUTO, TL_PATH_GEMV, TL_PATH_TC, TL_PATH_TCS = 0, 1, 2, 3
+TL_PATH_AUTO, TL_PATH_GEMV, TL_PATH_TC, TL_PATH_TCD = 0, 1, 2, 3
+TL_ACT_F16, TL_ACT_BF16 = 0, 1
+TL_FLAG_STATIC_WEIGHTS = 1
 
 _c_size = ctypes.c_size_t
 _i64 = ctypes.c_int64
@@ -76,16 +78,19 @@ _tl_pack = _sig("tl_pack", ctypes.c_int, [_W, _i64, _i64, _vp, _vp, _vp])
 _tl_unpack = _sig("tl_unpack", ctypes.c_int, [_W, _i64, _i64, _vp, _vp, _vp])
 _tl_transform_weights = _sig("tl_transform_weights", ctypes.c_int, [_W, _i64, _i64, _vp, _vp, _vp])
 _tl_untransform_weights = _sig("tl_untransform_weights", ctypes.c_int, [_W, _i64, _i64, _vp, _vp, _vp])
-_tl_matmul_workspace_bytes = _sig("tl_matmul_workspace_bytes", _c_size, [_W, _i64, _i64, _i64, _i32])
+_A = ctypes.c_int  # tl_atype
+_u32 = ctypes.c_uint32
+_tl_matmul_workspace_bytes = _sig("tl_matmul_workspace_bytes", _c_size, [_W, _A, _i64, _i64, _i64, _i32])
 _tl_matmul = _sig("tl_matmul", ctypes.c_int,
-                  [_W, _i64, _i64, _i64, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _c_size, _vp])
+                  [_W, _A, _i64, _i64, _i64, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _c_size, _vp])
 _tl_matmul_ex = _sig("tl_matmul_ex", ctypes.c_int,
-                     [_W, _i64, _i64, _i64, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _c_size, _i32, _i32,
-                      _vp])
+                     [_W, _A, _i64, _i64, _i64, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _c_size, _i32, _i32,
+                      _u32, _vp])
 _tl_matmul_hostio = _sig("tl_matmul_hostio", ctypes.c_int,
-                         [_W, _i64, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_size, _vp])
+                         [_W, _A, _i64, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_size, _u32,
+                          _vp])
 _tl_matmul_plan = _sig("tl_matmul_plan", ctypes.c_int,
-                       [_W, _i64, _i64, _i64, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32)])
+                       [_W, _A, _i64, _i64, _i64, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32)])
 _tl_dequant = _sig("tl_dequant", ctypes.c_int, [_W, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _vp])
 _tl_status_str = _sig("tl_status_str", ctypes.c_char_p, [ctypes.c_int])
 _tl_last_error = _sig("tl_last_error", ctypes.c_char_p, [])
@@ -135,8 +140,8 @@ def tl_format_version() -> int:
     return _tl_format_version()
 
 
-def tl_matmul_workspace_bytes(w: tl_wtype, M: int, N: int, K: int, group: int) -> int:
-    return _tl_matmul_workspace_bytes(w, M, N, K, group)
+def tl_matmul_workspace_bytes(w: tl_wtype, M: int, N: int, K: int, group: int, atype: int = TL_ACT_F16) -> int:
+    return _tl_matmul_workspace_bytes(w, atype, M, N, K, group)
 
 
 # ---- weight preparation ------------------------------------------------------------------
@@ -187,37 +192,45 @@ def alloc_workspace(w: tl_wtype, M: int, N: int, K: int, group: int, device="cud
     return torch.zeros(tl_matmul_workspace_bytes(w, M, N, K, group), dtype=torch.uint8, device=device)
 
 
+def _atype(A: torch.Tensor) -> int:
+    if A.dtype == torch.float16:
+        return TL_ACT_F16
+    if A.dtype == torch.bfloat16:
+        return TL_ACT_BF16
+    raise ValueError(f"activations must be fp16 or bf16, got {A.dtype}")
+
+
 def tl_matmul(w: tl_wtype, M: int, N: int, K: int, group: int, A: torch.Tensor, w_t: torch.Tensor,
               scales: torch.Tensor, zeros: torch.Tensor | None, Y: torch.Tensor, workspace: torch.Tensor,
               lda: int | None = None, ldy: int | None = None, stream=None) -> torch.Tensor:
-    _check(_tl_matmul(w, M, N, K, group, _ptr(A), lda if lda is not None else K, _ptr(w_t), _ptr(scales),
-                      _ptr(zeros), _ptr(Y), ldy if ldy is not None else N, _ptr(workspace), workspace.numel(),
-                      _stream(stream)), "tl_matmul")
+    _check(_tl_matmul(w, _atype(A), M, N, K, group, _ptr(A), lda if lda is not None else K, _ptr(w_t),
+                      _ptr(scales), _ptr(zeros), _ptr(Y), ldy if ldy is not None else N, _ptr(workspace),
+                      workspace.numel(), _stream(stream)), "tl_matmul")
     return Y
 
 
 def tl_matmul_ex(w: tl_wtype, M: int, N: int, K: int, group: int, A: torch.Tensor, w_t: torch.Tensor,
                  scales: torch.Tensor, zeros: torch.Tensor | None, Y: torch.Tensor, workspace: torch.Tensor,
                  path: int = TL_PATH_AUTO, splits: int = 0, lda: int | None = None, ldy: int | None = None,
-                 stream=None) -> torch.Tensor:
-    _check(_tl_matmul_ex(w, M, N, K, group, _ptr(A), lda if lda is not None else K, _ptr(w_t), _ptr(scales),
-                         _ptr(zeros), _ptr(Y), ldy if ldy is not None else N, _ptr(workspace), workspace.numel(),
-                         path, splits, _stream(stream)), "tl_matmul_ex")
+                 flags: int = 0, stream=None) -> torch.Tensor:
+    _check(_tl_matmul_ex(w, _atype(A), M, N, K, group, _ptr(A), lda if lda is not None else K, _ptr(w_t),
+                         _ptr(scales), _ptr(zeros), _ptr(Y), ldy if ldy is not None else N, _ptr(workspace),
+                         workspace.numel(), path, splits, flags, _stream(stream)), "tl_matmul_ex")
     return Y
 
 
 def tl_matmul_hostio(w: tl_wtype, M: int, N: int, K: int, group: int, A_host: torch.Tensor, A_dev: torch.Tensor,
                      w_t: torch.Tensor, scales: torch.Tensor, zeros: torch.Tensor | None, Y_dev: torch.Tensor,
-                     Y_host: torch.Tensor, workspace: torch.Tensor, stream=None) -> torch.Tensor:
+                     Y_host: torch.Tensor, workspace: torch.Tensor, flags: int = 0, stream=None) -> torch.Tensor:
     if A_host.is_cuda or Y_host.is_cuda:
         raise ValueError("A_host / Y_host must be host tensors")
-    _check(_tl_matmul_hostio(w, M, N, K, group, A_host.data_ptr(), _ptr(A_dev), _ptr(w_t), _ptr(scales),
-                             _ptr(zeros), _ptr(Y_dev), Y_host.data_ptr(), _ptr(workspace), workspace.numel(),
-                             _stream(stream)), "tl_matmul_hostio")
+    _check(_tl_matmul_hostio(w, _atype(A_dev), M, N, K, group, A_host.data_ptr(), _ptr(A_dev), _ptr(w_t),
+                             _ptr(scales), _ptr(zeros), _ptr(Y_dev), Y_host.data_ptr(), _ptr(workspace),
+                             workspace.numel(), flags, _stream(stream)), "tl_matmul_hostio")
     return Y_host
 
 
-def tl_matmul_plan(w: tl_wtype, M: int, N: int, K: int, group: int) -> tuple[int, int]:
+def tl_matmul_plan(w: tl_wtype, M: int, N: int, K: int, group: int, atype: int = TL_ACT_F16) -> tuple[int, int]:
     p, s = _i32(0), _i32(0)
-    _check(_tl_matmul_plan(w, M, N, K, group, ctypes.byref(p), ctypes.byref(s)), "tl_matmul_plan")
+    _check(_tl_matmul_plan(w, atype, M, N, K, group, ctypes.byref(p), ctypes.byref(s)), "tl_matmul_plan")
     return p.value, s.value

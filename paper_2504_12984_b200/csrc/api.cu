@@ -3,6 +3,9 @@
 // host-buffer end-to-end call and the error strings.
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "api_util.cuh"
 #include "paths.cuh"
@@ -18,6 +21,27 @@ void set_error(const char* fmt, ...) {
   va_end(ap);
 }
 
+int prepare_kernel(const void* fn, int smem_bytes, int threads) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> occ;  // (kernel, device) -> CTAs per SM
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    set_error("cudaGetDevice failed");
+    return 0;
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = occ.find({fn, dev});
+  if (it != occ.end()) return it->second;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes) != cudaSuccess) {
+    set_error("cudaFuncSetAttribute(MaxDynamicSharedMemorySize=%d) failed on device %d", smem_bytes, dev);
+    return 0;
+  }
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem_bytes) != cudaSuccess || n < 1) n = 1;
+  occ[{fn, dev}] = n;
+  return n;
+}
+
 // Workspace: [semaphores: 64 KiB][partials ...]
 constexpr size_t kSemBytes = 64 * 1024;
 
@@ -31,13 +55,12 @@ static int env_int(const char* name, int dflt) {
 // from the measured sweep.
 static int choose_path(tl_wtype w, int64_t M, int32_t G) {
   const int forced = env_int("TL_FORCE_PATH", 0);
-  if (forced == TL_PATH_GEMV || forced == TL_PATH_TC || forced == TL_PATH_TCS) return forced;
-  if (!tc_available()) return TL_PATH_GEMV;
+  if (forced == TL_PATH_GEMV || forced == TL_PATH_TC || forced == TL_PATH_TCD) return forced;
   (void)w;
   // measured on B200: the tensor-core decode kernel (tcd) for M <= 16 with a group
   // that is a multiple of 128 (it beats the CUDA-core GEMV from M = 1), the CUDA-core GEMV for the
   // remaining decode shapes (G = 32, 64), the tcgen05 GEMM above M = 16
-  if (tcs_eligible(M, G)) return TL_PATH_TCS;
+  if (tcd_eligible(M, G)) return TL_PATH_TCD;
   if (M <= 1) return TL_PATH_GEMV;
   return TL_PATH_TC;
 }
@@ -66,19 +89,21 @@ const char* tl_status_str(tl_status s) {
 
 const char* tl_last_error(void) { return g_err; }
 
-size_t tl_matmul_workspace_bytes(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t group) {
+size_t tl_matmul_workspace_bytes(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group) {
   (void)w;
   (void)group;
+  if (a != TL_ACT_F16) return 0;
   if (M <= 0 || N <= 0 || K <= 0) return kSemBytes;
   size_t g = gemv_workspace_bytes(M, N, K);
   size_t t = tc_workspace_bytes(M, N, K);
-  size_t ts = tcs_workspace_bytes(M, N, K);
+  size_t ts = tcd_workspace_bytes(M, N, K);
   if (ts > t) t = ts;
   return kSemBytes + (g > t ? g : t);
 }
 
-tl_status tl_matmul_plan(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t group, int32_t* path_out,
-                         int32_t* splits_out) {
+tl_status tl_matmul_plan(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group,
+                         int32_t* path_out, int32_t* splits_out) {
+  if (a != TL_ACT_F16) return fail(TL_EUNSUPPORTED, "activation type %d is not supported by this build", (int)a);
   (void)N;
   (void)K;
   (void)group;
@@ -87,11 +112,17 @@ tl_status tl_matmul_plan(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t gr
   return TL_OK;
 }
 
-tl_status tl_matmul_ex(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t group, const void* A, int64_t lda,
-                       const void* w_t, const void* scales, const void* zeros, void* Y, int64_t ldy,
-                       void* workspace, size_t workspace_bytes, int32_t path, int32_t splits, void* stream) {
+tl_status tl_matmul_ex(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group, const void* A,
+                       int64_t lda, const void* w_t, const void* scales, const void* zeros, void* Y, int64_t ldy,
+                       void* workspace, size_t workspace_bytes, int32_t path, int32_t splits, uint32_t flags,
+                       void* stream) {
   tl_status st;
   if ((st = check_wtype(w)) != TL_OK) return st;
+  if (a != TL_ACT_F16)
+    return fail(TL_EUNSUPPORTED, "activation type %d is not supported by this build (TL_ACT_F16 only)", (int)a);
+  if (flags & ~TL_FLAG_STATIC_WEIGHTS) return fail(TL_EINVAL_SHAPE, "unknown flags 0x%x", flags);
+  if (path < TL_PATH_AUTO || path > TL_PATH_TCD) return fail(TL_EUNSUPPORTED, "unknown path %d", path);
+  if (splits < 0) return fail(TL_EINVAL_SHAPE, "splits=%d < 0", splits);
   if ((st = check_kn(K, N)) != TL_OK) return st;
   if ((st = check_group(K, group)) != TL_OK) return st;
   if (M < 0) return fail(TL_EINVAL_SHAPE, "M=%lld < 0", (long long)M);
@@ -103,12 +134,12 @@ tl_status tl_matmul_ex(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t grou
   if (!aligned16(A) || !aligned16(w_t) || !aligned16(scales) || !aligned16(Y) || (zeros && !aligned16(zeros)) ||
       (lda * 2) % 16 || (ldy * 2) % 16)
     return fail(TL_EALIGN, "pointers and row strides must be 16-byte aligned");
-  const size_t need = tl_matmul_workspace_bytes(w, M, N, K, group);
+  const size_t need = tl_matmul_workspace_bytes(w, a, M, N, K, group);
   if (!workspace || workspace_bytes < need)
     return fail(TL_EWORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
   if (!aligned16(workspace)) return fail(TL_EALIGN, "workspace must be 16-byte aligned");
   if (path == TL_PATH_AUTO) path = choose_path(w, M, group);
-  if (path == TL_PATH_TCS && !tcs_eligible(M, group)) path = TL_PATH_TC;
+  if (path == TL_PATH_TCD && !tcd_eligible(M, group)) path = TL_PATH_TC;
   int* sem = reinterpret_cast<int*>(workspace);
   float* partial = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(workspace) + kSemBytes);
   cudaStream_t s = as_stream(stream);
@@ -117,9 +148,9 @@ tl_status tl_matmul_ex(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t grou
       // the CUDA-core path handles up to 16 rows per launch
       for (int64_t m0 = 0; m0 < M; m0 += 16) {
         const int64_t mm = (M - m0) < 16 ? (M - m0) : 16;
-        st = tl_matmul_ex(w, mm, N, K, group, reinterpret_cast<const __half*>(A) + m0 * lda, lda, w_t, scales, zeros,
-                          reinterpret_cast<__half*>(Y) + m0 * ldy, ldy, workspace, workspace_bytes, TL_PATH_GEMV,
-                          splits, stream);
+        st = tl_matmul_ex(w, a, mm, N, K, group, reinterpret_cast<const __half*>(A) + m0 * lda, lda, w_t, scales,
+                          zeros, reinterpret_cast<__half*>(Y) + m0 * ldy, ldy, workspace, workspace_bytes,
+                          TL_PATH_GEMV, splits, flags, stream);
         if (st != TL_OK) return st;
       }
       return TL_OK;
@@ -142,39 +173,44 @@ tl_status tl_matmul_ex(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t grou
     p.magic = 0x64006400u;
     return gemv_dispatch(w, p, splits > 0 ? splits : env_int("TL_GRID", 0), s);
   }
+  if (path == TL_PATH_TCD) {
+    tl_status r = tcd_matmul(w, M, N, K, group, reinterpret_cast<const __half*>(A), lda,
+                             reinterpret_cast<const uint8_t*>(w_t), reinterpret_cast<const __half*>(scales),
+                             reinterpret_cast<const __half*>(zeros), reinterpret_cast<__half*>(Y), ldy, partial, sem,
+                             splits, (flags & TL_FLAG_STATIC_WEIGHTS) != 0, s);
+    if (r != TL_ENOFIT) return r;
+    // the decode kernel's stage ring does not fit shared memory for this shape: batched path
+    path = TL_PATH_TC;
+  }
   if (path == TL_PATH_TC) {
-    if (!tc_available()) return fail(TL_EUNSUPPORTED, "tensor-core path not built");
     return tc_matmul(w, M, N, K, group, reinterpret_cast<const __half*>(A), lda,
                      reinterpret_cast<const uint8_t*>(w_t), reinterpret_cast<const __half*>(scales),
                      reinterpret_cast<const __half*>(zeros), reinterpret_cast<__half*>(Y), ldy, partial, sem,
                      splits, s);
   }
-  if (path == TL_PATH_TCS) {
-    return tcs_matmul(w, M, N, K, group, reinterpret_cast<const __half*>(A), lda,
-                      reinterpret_cast<const uint8_t*>(w_t), reinterpret_cast<const __half*>(scales),
-                      reinterpret_cast<const __half*>(zeros), reinterpret_cast<__half*>(Y), ldy, partial, sem,
-                      splits, s);
-  }
   return fail(TL_EUNSUPPORTED, "unknown path %d", path);
 }
 
-tl_status tl_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t group, const void* A, int64_t lda,
-                    const void* w_t, const void* scales, const void* zeros, void* Y, int64_t ldy, void* workspace,
-                    size_t workspace_bytes, void* stream) {
-  return tl_matmul_ex(w, M, N, K, group, A, lda, w_t, scales, zeros, Y, ldy, workspace, workspace_bytes,
-                      TL_PATH_AUTO, 0, stream);
+tl_status tl_matmul(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group, const void* A,
+                    int64_t lda, const void* w_t, const void* scales, const void* zeros, void* Y, int64_t ldy,
+                    void* workspace, size_t workspace_bytes, void* stream) {
+  return tl_matmul_ex(w, a, M, N, K, group, A, lda, w_t, scales, zeros, Y, ldy, workspace, workspace_bytes,
+                      TL_PATH_AUTO, 0, 0u, stream);
 }
 
-tl_status tl_matmul_hostio(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t group, const void* A_host,
-                           void* A_dev, const void* w_t, const void* scales, const void* zeros, void* Y_dev,
-                           void* Y_host, void* workspace, size_t workspace_bytes, void* stream) {
+tl_status tl_matmul_hostio(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group,
+                           const void* A_host, void* A_dev, const void* w_t, const void* scales, const void* zeros,
+                           void* Y_dev, void* Y_host, void* workspace, size_t workspace_bytes, uint32_t flags,
+                           void* stream) {
   if (M == 0) return TL_OK;
+  if (a != TL_ACT_F16)
+    return fail(TL_EUNSUPPORTED, "activation type %d is not supported by this build (TL_ACT_F16 only)", (int)a);
   if (!A_host || !A_dev || !Y_dev || !Y_host) return fail(TL_ENULL, "tl_matmul_hostio: NULL pointer");
   cudaStream_t s = as_stream(stream);
   if (cudaMemcpyAsync(A_dev, A_host, (size_t)(M * K * 2), cudaMemcpyHostToDevice, s) != cudaSuccess)
     return fail(TL_ECUDA, "H2D copy of A failed");
-  tl_status st = tl_matmul(w, M, N, K, group, A_dev, K, w_t, scales, zeros, Y_dev, N, workspace, workspace_bytes,
-                           stream);
+  tl_status st = tl_matmul_ex(w, a, M, N, K, group, A_dev, K, w_t, scales, zeros, Y_dev, N, workspace,
+                              workspace_bytes, TL_PATH_AUTO, 0, flags, stream);
   if (st != TL_OK) return st;
   if (cudaMemcpyAsync(Y_host, Y_dev, (size_t)(M * N * 2), cudaMemcpyDeviceToHost, s) != cudaSuccess)
     return fail(TL_ECUDA, "D2H copy of Y failed");

@@ -53,6 +53,12 @@ inline tl_status check_group(int64_t K, int32_t G) {
   return TL_OK;
 }
 
+// Per-(kernel, device) one-time preparation: opts `fn` into `smem_bytes` of dynamic
+// shared memory on the CURRENT device and returns its resident CTAs per SM there (occupancy).
+// Function attributes are per device context, so the cache is keyed on (fn, device); it is
+// guarded by a mutex (the C ABI is thread-safe).  Returns 0 on a CUDA error (tl_last_error set).
+int prepare_kernel(const void* fn, int smem_bytes, int threads);
+
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }

@@ -5,13 +5,14 @@
 namespace tl {
 
 // ---------------------------------------------------------------------------------
-// dequant hook: thread per (tile, column); the column run's segment words are loaded with
-// the same 16-byte vectors and unpacked with the same pair_value<> the tensor-core
-// dequant warps use, then scaled EXACTLY in fp32.
+// dequant hook: thread per (tile, column); the column's words are loaded with the same 16-byte
+// vectors and unpacked with the same extract_pair<> the kernels use, then scaled EXACTLY in fp32:
+//   ints:   (x & mask) | 0x6400 = 1024 + u*2^P;  HFMA2(x, 2^-P, -(2^(10-P) + z)) = u - z exactly
+//   floats: the field placement is value(code) * 2^(bias-15) exactly; * 2^(15-bias) in fp32
 template <class F>
 __global__ void dequant_kernel(const uint8_t* __restrict__ wt, const __half* __restrict__ scales,
                                const __half* __restrict__ zeros, float* __restrict__ out, int64_t K, int64_t N,
-                               int G, uint32_t magic) {
+                               int G) {
   const int64_t KT = K / kBK;
   const int64_t tile = blockIdx.x;
   const int nl = threadIdx.x;
@@ -20,43 +21,47 @@ __global__ void dequant_kernel(const uint8_t* __restrict__ wt, const __half* __r
   const uint8_t* tb = wt + tile * (int64_t)tile_bytes(F::bits);
   uint32_t words[4 * F::bits];
 #pragma unroll
-  for (int s = 0; s < F::nseg; ++s) {
-    const int w = seg_width(F::bits, s), base = seg_base(F::bits, s);
-#pragma unroll
-    for (int v = 0; v < w; ++v) {
-      const uint4 x = ld_nc_v4(tb + 2048 * base + (v * 128 + nl) * 16);
-      words[4 * base + 4 * v + 0] = x.x;
-      words[4 * base + 4 * v + 1] = x.y;
-      words[4 * base + 4 * v + 2] = x.z;
-      words[4 * base + 4 * v + 3] = x.w;
-    }
+  for (int v = 0; v < F::bits; ++v) {
+    const uint4 x = ld_nc_v4(tb + (v * 128 + nl) * 16);
+    words[4 * v + 0] = x.x;
+    words[4 * v + 1] = x.y;
+    words[4 * v + 2] = x.z;
+    words[4 * v + 3] = x.w;
   }
-  PairConsts pc;
-  pc.magic = magic;
-  int gcur = -1;
-  float s = 0.f;
-  static_for<0, 64>([&](auto I) {
-    constexpr int i = decltype(I)::value;
-    const int64_t k = kt * kBK + 2 * i;
-    const int g = (int)(k / G);
-    if (g != gcur) {
-      gcur = g;
-      s = __half2float(scales[(int64_t)g * N + n]);
-      float z = 0.f;
-      if (F::kind == kUint && zeros) z = __half2float(zeros[(int64_t)g * N + n]);
-      if (F::kind == kInt) z = (float)(1 << (F::bits - 1));
-      make_pair_consts<F>(pc, z);
-    }
-    const float2 v = __half22float2(pair_value<F, i>(words, pc));
-    out[k * N + n] = v.x * s;          // (value - z) * s is exact in fp32 (reading R9)
-    out[(k + 1) * N + n] = v.y * s;
+  static_for<0, 2>([&](auto HH) {
+    constexpr int h = decltype(HH)::value;
+    uint32_t bw[2 * F::bits];
+#pragma unroll
+    for (int j = 0; j < 2 * F::bits; ++j) bw[j] = words[tile_word(h, j)];
+    static_for<0, 32>([&](auto I) {
+      constexpr int i = decltype(I)::value;
+      constexpr PairPlan pp = kPlan<F::kind, F::bits, F::exp>.pr[i];
+      const int64_t k = kt * kBK + 2 * (32 * h + i);
+      const int64_t g = k / G;
+      const float s = __half2float(scales[g * N + n]);
+      float2 v;
+      if constexpr (F::kind != kFloat) {
+        float z = (float)(1 << (F::bits - 1));
+        if constexpr (F::kind == kUint) z = zeros ? __half2float(zeros[g * N + n]) : 0.f;
+        const __half c = __float2half_rn(-(float)(1 << (10 - pp.P)) - z);  // integer < 2048: exact
+        const uint32_t x = extract_pair<F, i>(bw, 0x64006400u);
+        v = __half22float2(__hfma2(u32_as_h2(x), u32_as_h2(h2_pow2_neg<pp.P>()), __halves2half2(c, c)));
+      } else {
+        const uint32_t x = extract_pair<F, i>(bw, 0u);
+        const float2 r = __half22float2(u32_as_h2(x));
+        constexpr float up = (float)(1 << (15 - F::bias));
+        v = make_float2(r.x * up, r.y * up);
+      }
+      out[k * N + n] = v.x * s;          // (value - z) * s is exact in fp32 (reading R9)
+      out[(k + 1) * N + n] = v.y * s;
+    });
   });
 }
 
 template <class F>
 void launch_dequant(const uint8_t* wt, const __half* scales, const __half* zeros, float* out, int64_t K, int64_t N,
                     int G, unsigned tiles, cudaStream_t st) {
-  dequant_kernel<F><<<tiles, kBN, 0, st>>>(wt, scales, zeros, out, K, N, G, 0x64006400u);
+  dequant_kernel<F><<<tiles, kBN, 0, st>>>(wt, scales, zeros, out, K, N, G);
 }
 
 }  // namespace tl

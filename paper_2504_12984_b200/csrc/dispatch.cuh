@@ -39,13 +39,4 @@ inline bool dispatch_format(int kind, int bits, int exp, Fn&& f) {
   }
 }
 
-// compile-time loop
-template <int I, int N, class Fn>
-__device__ __forceinline__ void static_for(Fn&& f) {
-  if constexpr (I < N) {
-    f(std::integral_constant<int, I>{});
-    static_for<I + 1, N>(f);
-  }
-}
-
 }  // namespace tl

@@ -41,29 +41,53 @@ __global__ void unpack_kernel(const uint8_t* __restrict__ in, uint8_t* __restric
 }
 
 // ---------------------------------------------------------------------------------
-// transform: thread per output 32-bit word of the v1 layout (common.cuh).
+// Layout v2 tables (common.cuh make_plan), built on the host from the same plan the kernels
+// unpack with, passed by value:
+//   inv[j*16 + q] = 8*i + cb : bit q of each half of block-local word j holds code bit cb of pair i
+//   fwd[8*i + cb] = 16*j + q : the inverse
+struct LayoutTables {
+  uint8_t inv[256];
+  uint8_t fwd[256];
+};
+
+static LayoutTables layout_tables(tl_wtype w) {
+  LayoutTables t{};
+  const int b = w.bits, E = w.kind == 2 ? w.exp_bits : 0, M = b - 1 - E;
+  const BlockPlan pl = make_plan(w.kind, b, E);
+  for (int i = 0; i < 32; ++i)
+    for (int k = 0; k < pl.pr[i].nt; ++k) {
+      const Term& tm = pl.pr[i].t[k];
+      for (int fb = 0; fb < 16; ++fb)
+        if ((tm.mask >> fb) & 1) {
+          const int cb = w.kind == 2 ? (fb == 15 ? b - 1 : fb - (10 - M)) : fb - pl.pr[i].P;
+          const int q = fb + tm.shift;
+          t.inv[tm.word * 16 + q] = (uint8_t)(8 * i + cb);
+          t.fwd[8 * i + cb] = (uint8_t)(16 * tm.word + q);
+        }
+    }
+  return t;
+}
+
+// transform: thread per output 32-bit word.  Word r of 16-byte vector v of column nl of a tile
+// is block h = r/2, block-local word j = 2v + (r&1); its bit 16*hh + q holds code bit cb of
+// pair i (inv table), i.e. of element k = 2*(32h + i) + hh.
 __global__ void transform_kernel(const uint8_t* __restrict__ bs, uint32_t* __restrict__ out, int64_t K, int64_t N,
-                                 int bits, uint32_t flip_top, int64_t nwords) {
+                                 int bits, uint32_t flip_top, int64_t nwords, LayoutTables lt) {
   const int64_t KT = K / kBK;
   const int words_per_tile = 512 * bits;
   for (int64_t wi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; wi < nwords; wi += (int64_t)gridDim.x * blockDim.x) {
     const int64_t tile = wi / words_per_tile;
     const int wt = (int)(wi % words_per_tile);
     const int64_t nt = tile / KT, kt = tile % KT;
-    int s = 0;
-    while (wt >= 512 * (seg_base(bits, s) + seg_width(bits, s))) ++s;
-    const int w = seg_width(bits, s);
-    const int base = seg_base(bits, s);
-    const int ws = wt - 512 * base;
-    const int vi = ws >> 2, r = ws & 3;
+    const int vi = wt >> 2, r = wt & 3;
     const int v = vi >> 7, nl = vi & 127;
-    const int j = v * 4 + r;
-    const int per_word = 32 / w;
+    const int h = r >> 1, j = 2 * v + (r & 1);
     uint32_t word = 0;
     for (int q = 0; q < 32; ++q) {
-      const int h = q >> 4, qq = q & 15;
-      const int p = qq / w, cbit = base + qq % w;
-      const int kl = j * per_word + 2 * p + h;
+      const int hh = q >> 4;
+      const int e = lt.inv[j * 16 + (q & 15)];
+      const int i = e >> 3, cbit = e & 7;
+      const int kl = 2 * (32 * h + i) + hh;
       const int64_t k = kt * kBK + kl, n = nt * kBN + nl;
       const int64_t pos = (k * N + n) * bits + cbit;
       uint32_t bit = (bs[pos >> 3] >> (pos & 7)) & 1u;
@@ -76,26 +100,29 @@ __global__ void transform_kernel(const uint8_t* __restrict__ bs, uint32_t* __res
 
 // untransform: thread per output byte of the bitstream.
 __global__ void untransform_kernel(const uint8_t* __restrict__ wt, uint8_t* __restrict__ bs, int64_t K, int64_t N,
-                                   int bits, uint32_t flip_top, int64_t nbytes) {
+                                   int bits, uint32_t flip_top, int64_t nbytes, LayoutTables lt) {
   const int64_t KT = K / kBK;
   const int64_t total_bits = K * N * bits;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nbytes; j += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t jb = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; jb < nbytes; jb += (int64_t)gridDim.x * blockDim.x) {
     uint32_t byte = 0;
     for (int t = 0; t < 8; ++t) {
-      const int64_t pos = j * 8 + t;
+      const int64_t pos = jb * 8 + t;
       if (pos >= total_bits) break;
       const int64_t e = pos / bits;
       const int cbit = (int)(pos % bits);
       const int64_t k = e / N, n = e % N;
       const int64_t kt = k / kBK, nt = n / kBN;
-      int off, bit;
-      locate_bit(bits, (int)(k % kBK), (int)(n % kBN), cbit, &off, &bit);
+      const int kl = (int)(k % kBK), nl = (int)(n % kBN);
+      const int pair = kl >> 1, hh = kl & 1, h = pair >> 5, i = pair & 31;
+      const int f = lt.fwd[8 * i + cbit];
+      const int j = f >> 4, q = (f & 15) + 16 * hh;
+      const int off = ((j >> 1) * 128 + nl) * 16 + 4 * (2 * h + (j & 1)) + (q >> 3);
       const int64_t tile = nt * KT + kt;
-      uint32_t v = (wt[tile * (int64_t)tile_bytes(bits) + off] >> bit) & 1u;
+      uint32_t v = (wt[tile * (int64_t)tile_bytes(bits) + off] >> (q & 7)) & 1u;
       if (cbit == bits - 1) v ^= flip_top;
       byte |= v << t;
     }
-    bs[j] = (uint8_t)byte;
+    bs[jb] = (uint8_t)byte;
   }
 }
 
@@ -155,7 +182,7 @@ tl_status tl_transform_weights(tl_wtype w, int64_t K, int64_t N, const uint8_t* 
   if (!aligned16(w_t)) return fail(TL_EALIGN, "w_t must be 16-byte aligned");
   const int64_t nwords = K * N * w.bits / 32;
   transform_kernel<<<grid_for(nwords, 256), 256, 0, as_stream(stream)>>>(
-      bitstream, reinterpret_cast<uint32_t*>(w_t), K, N, w.bits, w.kind == 1 ? 1u : 0u, nwords);
+      bitstream, reinterpret_cast<uint32_t*>(w_t), K, N, w.bits, w.kind == 1 ? 1u : 0u, nwords, layout_tables(w));
   return check_launch("transform_kernel");
 }
 
@@ -167,7 +194,7 @@ tl_status tl_untransform_weights(tl_wtype w, int64_t K, int64_t N, const void* w
   if (!bitstream || !w_t) return fail(TL_ENULL, "tl_untransform_weights: NULL pointer");
   const int64_t nb = (int64_t)tl_packed_bytes(w, K, N);
   untransform_kernel<<<grid_for(nb, 256), 256, 0, as_stream(stream)>>>(
-      reinterpret_cast<const uint8_t*>(w_t), bitstream, K, N, w.bits, w.kind == 1 ? 1u : 0u, nb);
+      reinterpret_cast<const uint8_t*>(w_t), bitstream, K, N, w.bits, w.kind == 1 ? 1u : 0u, nb, layout_tables(w));
   return check_launch("untransform_kernel");
 }
 

@@ -17,8 +17,9 @@ tl_status gemv_dispatch(tl_wtype w, const GemvParams& p, int grid_req, cudaStrea
 }
 
 size_t gemv_workspace_bytes(int64_t M, int64_t N, int64_t K) {
-  // partial slots for at most 148*8 CTAs, 2 slots each, + one semaphore per n-tile
-  const int64_t grid = 148 * 8;
+  // partial slots for at most kGemvMaxCtas CTAs (the launch clamps its grid to it), 2 slots each,
+  // + one semaphore per n-tile
+  const int64_t grid = kGemvMaxCtas;
   return (size_t)(grid * 2 * (M > 16 ? 16 : M) * kBN * 4) + (size_t)((N / kBN) * 4) + 256;
 }
 

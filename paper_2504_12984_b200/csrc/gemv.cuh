@@ -10,9 +10,9 @@
 //     ring (mbarriers); a few stages behind, the same warp pre-scales the activations by
 //     2^-P per k and writes the sum of A over every 32-k sub-piece into the stage;
 //   * 256 consumer threads: thread (c, kh) owns column c of the tile and the k-half kh; it
-//     reads its column's segment words with 16-byte LDS; ONE LOP3 per pair of codes places
-//     them in the two fp16 lanes as u * 2^(P-24) (exact fp16 subnormals -- no conversion
-//     instruction at all), and FHFMA (fma.rn.f32.f16: fp16 x fp16 + fp32) accumulates
+//     reads its column's k-half block words with 8-byte LDS; one LOP3 per pair of codes (layout
+//     v2, common.cuh) places them in the two fp16 lanes as u * 2^(P-24) (exact fp16 subnormals --
+//     no conversion instruction at all), and FHFMA (fma.rn.f32.f16: fp16 x fp16 + fp32) accumulates
 //     u * A * 2^-24 exactly in fp32 (reading R10).  The zero point and the
 //     group scale are applied once per 32-k sub-piece: Y += s * (2^24 * acc - z * sum(A));
 //     float codes are placed on the fp16 exponent/mantissa fields (value * 2^(bias-15)) and
@@ -63,8 +63,8 @@ __device__ __forceinline__ void gemv_tile_half(const uint8_t* stage, int c, cons
                                                const uint16_t (&zc)[2], float (&tot)[MT]) {
   using L = GemvLayout<F, MT>;
   constexpr int B = F::bits;
-  uint32_t words[4 * B];
-  load_half_words<B, KH>(stage, c, words);
+  uint32_t bw[2 * B];
+  load_block_words<B, KH>(stage, c, bw);  // layout v2: k-half KH = block KH
   const __half* As = reinterpret_cast<const __half*>(stage + L::w_bytes);
   const float* Ss = reinterpret_cast<const float*>(stage + L::w_bytes + L::a_bytes);
   float acc[MT];
@@ -73,7 +73,8 @@ __device__ __forceinline__ void gemv_tile_half(const uint8_t* stage, int c, cons
   static_for<0, 32>([&](auto II) {
     constexpr int ii = decltype(II)::value;
     constexpr int i = KH * 32 + ii;
-    const uint32_t wp = raw_pair_bits<F, i>(words);
+    // raw fields (no magic): ints u * 2^(P-24) (exact fp16 subnormal), floats value * 2^(bias-15)
+    const uint32_t wp = extract_pair<F, ii>(bw, 0u);
 #pragma unroll
     for (int m = 0; m < MT; ++m)
       acc[m] = fhfma2(wp, *reinterpret_cast<const uint32_t*>(As + m * kBK + 2 * i), acc[m]);
@@ -165,8 +166,9 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvParams p) {
       int P0 = 0, P1 = 0;
       static_for<0, 64>([&](auto II) {
         constexpr int i = decltype(II)::value;
-        if (i == 2 * lane) P0 = SubP<F::bits, i>::value;
-        if (i == 2 * lane + 1) P1 = SubP<F::bits, i>::value;
+        constexpr int Pi = kPlan<F::kind, F::bits, F::exp>.pr[i & 31].P;
+        if (i == 2 * lane) P0 = Pi;
+        if (i == 2 * lane + 1) P1 = Pi;
       });
       pre0 = __float2half2_rn(__int_as_float((127 - P0) << 23));
       pre1 = __float2half2_rn(__int_as_float((127 - P1) << 23));
@@ -318,14 +320,8 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvParams p) {
 template <class F, int MT>
 static tl_status launch_gemv_mt(const GemvParams& p0, int grid_req, cudaStream_t st) {
   using L = GemvLayout<F, MT>;
-  static int max_ctas = 0;  // per instantiation: resident CTAs per SM
-  if (max_ctas == 0) {
-    if (cudaFuncSetAttribute(gemv_kernel<F, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::smem) != cudaSuccess)
-      return fail(TL_ECUDA, "cudaFuncSetAttribute(gemv smem=%d)", L::smem);
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemv_kernel<F, MT>, kGemvThreads, L::smem);
-    max_ctas = occ > 0 ? occ : 1;
-  }
+  const int max_ctas = prepare_kernel(reinterpret_cast<const void*>(gemv_kernel<F, MT>), L::smem, kGemvThreads);
+  if (max_ctas == 0) return fail(TL_ECUDA, "gemv_kernel: %s", tl_last_error());
   int sms = 148;
   {
     int dev = 0;
@@ -334,6 +330,7 @@ static tl_status launch_gemv_mt(const GemvParams& p0, int grid_req, cudaStream_t
   }
   GemvParams p = p0;
   int grid = grid_req > 0 ? grid_req : sms * max_ctas;
+  if (grid > kGemvMaxCtas) grid = kGemvMaxCtas;  // the workspace holds partial slots for this many CTAs
   if (grid > p.units) grid = p.units;
   gemv_kernel<F, MT><<<grid, kGemvThreads, L::smem, st>>>(p);
   return check_launch("gemv_kernel");

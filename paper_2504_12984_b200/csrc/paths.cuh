@@ -24,15 +24,18 @@ struct GemvParams {
 tl_status gemv_dispatch(tl_wtype w, const GemvParams& p, int grid_req, cudaStream_t st);
 size_t gemv_workspace_bytes(int64_t M, int64_t N, int64_t K);
 
-bool tc_available();
+// CTAs the GEMV workspace holds partial slots for (the grid is clamped to it)
+constexpr int kGemvMaxCtas = 148 * 8;
+// internal status (never returned through the ABI): the decode kernel's ring does not fit
+constexpr tl_status TL_ENOFIT = (tl_status)100;
 size_t tc_workspace_bytes(int64_t M, int64_t N, int64_t K);
 tl_status tc_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, const __half* A, int64_t lda,
                     const uint8_t* wt, const __half* scales, const __half* zeros, __half* Y, int64_t ldy,
                     float* partial, int* sem, int grid_req, cudaStream_t st);
-bool tcs_eligible(int64_t M, int32_t G);
-size_t tcs_workspace_bytes(int64_t M, int64_t N, int64_t K);
-tl_status tcs_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, const __half* A, int64_t lda,
+bool tcd_eligible(int64_t M, int32_t G);
+size_t tcd_workspace_bytes(int64_t M, int64_t N, int64_t K);
+tl_status tcd_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, const __half* A, int64_t lda,
                      const uint8_t* wt, const __half* scales, const __half* zeros, __half* Y, int64_t ldy,
-                     float* partial, int* sem, int grid_req, cudaStream_t st);
+                     float* partial, int* sem, int grid_req, bool static_weights, cudaStream_t st);
 
 }  // namespace tl

@@ -22,19 +22,17 @@ static tl_status make_tmap_a(CUtensorMap* m, const __half* A, int64_t M, int64_t
 
 long long* g_trace = nullptr;  // debug: clock64 stamps of CTA 0 (TL_TRACE=1)
 
-bool tc_available() { return true; }
-
-bool tcs_eligible(int64_t M, int32_t G) { return M >= 1 && M <= kTcdNB && G >= kBK; }
+bool tcd_eligible(int64_t M, int32_t G) { return M >= 1 && M <= kTcdNB && G >= kBK; }
 
 static int env_dbg(const char* name) {
   const char* v = getenv(name);
   return v ? atoi(v) : 0;
 }
 
-// decode tensor-core path, v2 (tcd.cuh): every side input rides in the TMA stage
-static tl_status tcd_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, const __half* A, int64_t lda,
-                            const uint8_t* wt, const __half* scales, const __half* zeros, __half* Y, int64_t ldy,
-                            float* partial, int* sem, int grid_req, cudaStream_t st) {
+// decode tensor-core path (tcd.cuh): the weight tile and its scale / zero slices ride in one TMA stage
+tl_status tcd_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, const __half* A, int64_t lda,
+                     const uint8_t* wt, const __half* scales, const __half* zeros, __half* Y, int64_t ldy,
+                     float* partial, int* sem, int grid_req, bool static_weights, cudaStream_t st) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -55,35 +53,35 @@ static tl_status tcd_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t
   p.partial = partial;
   p.sem = sem;
   p.dbg = env_dbg("TL_TCD_DBG");
+  p.static_w = static_weights ? 1 : 0;
+  p.magic = 0x64006400u;
   if (getenv("TL_TRACE")) {
     static int launches = 0;  // two trace buffers, alternating per launch (back-to-back overlap)
     if (!g_trace) cudaMalloc(&g_trace, 2 * 16 * 256 * sizeof(long long));
     p.trace = g_trace + (launches++ & 1) * 16 * 256;
   }
+  int grid = grid_req > 0 ? grid_req : sms;
+  if (grid > 160) grid = 160;
+  if (grid > p.units) grid = p.units;
   const uint32_t wb = (uint32_t)tile_bytes(w.bits);
   p.w_off = 0;
   p.s_off = p.w_off + wb;
   p.z_off = p.s_off + 256;
-  p.a_off = p.z_off + 256;
-  p.stage_bytes = (p.a_off + 127) & ~127u;
+  p.stage_bytes = (p.z_off + 256 + 127) & ~127u;
   const uint32_t red = (uint32_t)kTcdNG * (uint32_t)M * kBN * 4;
   const uint32_t opb = kTcdNOP * kTcdOpBytes;
-  const uint32_t sums = (uint32_t)(K / kBK) * (M <= 1 ? 1u : (uint32_t)kTcdNB) * 4;
-  const uint32_t fixed = 1024 /*align*/ + opb + 1024 + red + sums + 1024 /*barriers, tmem slot, flags*/;
+  const uint64_t fixed = 1024 /*align*/ + (uint64_t)opb + 1024 + red + 1024 /*barriers, tmem slot, flags*/;
+  if (fixed + (uint64_t)kTcdNOP * p.stage_bytes > 227u * 1024u)
+    return TL_ENOFIT;  // caller falls back to the batched path
   int ns = (int)((227u * 1024u - fixed) / p.stage_bytes);
   if (ns > 32) ns = 32;
   if (env_dbg("TL_TCD_NS") > 0 && env_dbg("TL_TCD_NS") < ns) ns = env_dbg("TL_TCD_NS");
-  if (ns < kTcdNOP) return fail(TL_EUNSUPPORTED, "decode tensor-core stage does not fit shared memory");
   p.ns = ns;
   p.op_off = ((uint32_t)ns * p.stage_bytes + 1023) & ~1023u;
   p.red_off = p.op_off + opb;
-  p.sums_off = p.red_off + red;
-  p.bar_off = (p.sums_off + sums + 15) & ~15u;
+  p.bar_off = (p.red_off + red + 15) & ~15u;
   const uint32_t smem = p.bar_off + (3 * ns + kTcdNOP + 2 * kTcdNW + 2 * kTcdNACC) * 8 + 32 + 1024;
-  if (smem > 227 * 1024) return fail(TL_EUNSUPPORTED, "decode tensor-core tile does not fit shared memory");
-  int grid = grid_req > 0 ? grid_req : sms;
-  if (grid > 160) grid = 160;
-  if (grid > p.units) grid = p.units;
+  if (smem > 227 * 1024) return TL_ENOFIT;
   CUtensorMap tmap;
   tl_status s = make_tmap_a(&tmap, A, M, K, lda, kTcdNB);
   if (s != TL_OK) return s;
@@ -95,17 +93,11 @@ static tl_status tcd_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t
   return s;
 }
 
-size_t tcs_workspace_bytes(int64_t M, int64_t N, int64_t K) {
+size_t tcd_workspace_bytes(int64_t M, int64_t N, int64_t K) {
   (void)M;
   (void)N;
   (void)K;
   return (size_t)160 * 2 * kTcdNB * 128 * 4;
-}
-
-tl_status tcs_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, const __half* A, int64_t lda,
-                     const uint8_t* wt, const __half* scales, const __half* zeros, __half* Y, int64_t ldy,
-                     float* partial, int* sem, int grid_req, cudaStream_t st) {
-  return tcd_matmul(w, M, N, K, G, A, lda, wt, scales, zeros, Y, ldy, partial, sem, grid_req, st);
 }
 
 constexpr int kTcMaxCtas = 160;

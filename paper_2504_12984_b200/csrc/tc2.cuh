@@ -14,8 +14,9 @@
 //               accumulating the whole K range of an n-tile in one TMEM accumulator.
 //   warps 2..13 three dequant groups of 4 warps (warp%4 = TMEM lane quarter); group g handles
 //               tiles t = g, g+3, ... into its two TMEM W^T slots (double buffer): LDS of the
-//               segment words, LOP3 + HFMA2 (magic number) -> exact (u - z) / value(code) fp16
-//               pairs (pair_value), HMUL2 by the group scale (reading R9), tcgen05.st.  The same
+//               column's words, LOP3 (layout v2, common.cuh) + HFMA2 (magic number) -> exact
+//               (u - z) / value(code) fp16 pairs, HMUL2 by the group scale (reading R9),
+//               tcgen05.st.  The same
 //               warps run the epilogue (tcgen05.ld -> fp16 -> Y, or a stream-K partial with a
 //               deterministic fixup) at the end of every 128-column n-tile.
 // Scales / zeros are read by the dequant threads straight from global memory, PF tiles ahead.
@@ -75,38 +76,71 @@ __device__ __forceinline__ uint64_t tc2_sw128_desc(uint32_t saddr) {
   return d;
 }
 
-// Dequantize row n of one tile (64 pairs) into a TMEM W^T slot; scales / zeros of the tile's
-// (up to four) 32-k sub-pieces come in sc[4] / zc[4] (fp16 bits).
+// is P the field position of some pair of the format's plan (ints)?
+template <class F>
+__host__ __device__ constexpr bool tc2_plan_uses_p(int P) {
+  for (int i = 0; i < 32; ++i)
+    if (kPlan<F::kind, F::bits, F::exp>.pr[i].P == P) return true;
+  return false;
+}
+
+// Dequantize row n of one tile (64 pairs, layout v2) into a TMEM W^T slot; scales / zeros of the
+// tile's (up to four) 32-k sub-pieces come in sc[4] / zc[4] (fp16 bits).
+//   ints:   LOP3(s) -> 1024 + u*2^P (magic form); HFMA2(x, 2^-P, -(2^(10-P) + z)) = u - z exactly;
+//           HMUL2 by s (one fp16 rounding, reading R9)
+//   floats: LOP3(s) -> value(code) * 2^(bias-15) exactly; HMUL2 by 2^(15-bias) (exact), HMUL2 by s
 template <class F>
 __device__ __forceinline__ void tc2_dequant_tile(uint32_t wtile, int n, uint32_t tslot, uint32_t magic,
                                                  const uint16_t (&sc)[4], const uint16_t (&zc)[4]) {
   constexpr int B = F::bits;
   uint32_t words[4 * B];
 #pragma unroll
-  for (int s = 0; s < num_segs(B); ++s) {
-    const int w = seg_width(B, s), base = seg_base(B, s);
-#pragma unroll
-    for (int v = 0; v < w; ++v) {
-      const uint4 x = lds128(wtile + 2048 * base + (v * 128 + n) * 16);
-      words[4 * base + 4 * v + 0] = x.x;
-      words[4 * base + 4 * v + 1] = x.y;
-      words[4 * base + 4 * v + 2] = x.z;
-      words[4 * base + 4 * v + 3] = x.w;
-    }
+  for (int v = 0; v < B; ++v) {
+    const uint4 x = lds128(wtile + (v * 128 + n) * 16);
+    words[4 * v + 0] = x.x;
+    words[4 * v + 1] = x.y;
+    words[4 * v + 2] = x.z;
+    words[4 * v + 3] = x.w;
   }
   static_for<0, 4>([&](auto CC) {
     constexpr int c = decltype(CC)::value;  // 16 pairs = one 32-k sub-piece = 16 TMEM columns
-    PairConsts pc;
-    pc.magic = magic;
-    float z = 0.f;
-    if constexpr (F::kind == kUint) z = __half2float(__ushort_as_half(zc[c]));
-    if constexpr (F::kind == kInt) z = (float)(1 << (B - 1));
-    make_pair_consts<F>(pc, z);
+    constexpr int h = c >> 1;
+    uint32_t bw[2 * B];
+#pragma unroll
+    for (int j = 0; j < 2 * B; ++j) bw[j] = words[tile_word(h, j)];
     const __half2 s2 = u32_as_h2((uint32_t)sc[c] | ((uint32_t)sc[c] << 16));
+    uint32_t cp[10];
+    if constexpr (F::kind != kFloat) {
+      uint32_t zneg;
+      if constexpr (F::kind == kUint) {
+        const uint32_t zb = (uint32_t)zc[c] ^ 0x8000u;
+        zneg = zb | (zb << 16);
+      } else {
+        constexpr uint32_t zb = 0x8000u | ((uint32_t)(B - 1 + 15) << 10);  // -2^(b-1)
+        zneg = zb | (zb << 16);
+      }
+      static_for<0, 10>([&](auto PP) {
+        constexpr int P = decltype(PP)::value;
+        if constexpr (tc2_plan_uses_p<F>(P)) {
+          constexpr uint32_t k = 0x8000u | ((uint32_t)(25 - P) << 10);  // fp16 -2^(10-P)
+          cp[P] = h2_as_u32(__hadd2(u32_as_h2(zneg), u32_as_h2(k | (k << 16))));
+        }
+      });
+    }
     uint32_t r[16];
     static_for<0, 16>([&](auto II) {
       constexpr int ii = decltype(II)::value;
-      r[ii] = h2_as_u32(__hmul2(pair_value<F, c * 16 + ii>(words, pc), s2));
+      constexpr int i = (c & 1) * 16 + ii;  // pair within the block
+      if constexpr (F::kind != kFloat) {
+        constexpr int P = kPlan<F::kind, F::bits, F::exp>.pr[i].P;
+        const uint32_t x = extract_pair<F, i>(bw, magic);
+        const __half2 v = __hfma2(u32_as_h2(x), u32_as_h2(h2_pow2_neg<P>()), u32_as_h2(cp[P]));
+        r[ii] = h2_as_u32(__hmul2(v, s2));
+      } else {
+        constexpr uint32_t e = (uint32_t)(30 - F::bias) << 10;  // fp16 bits of 2^(15-bias)
+        const uint32_t x = extract_pair<F, i>(bw, 0u);
+        r[ii] = h2_as_u32(__hmul2(__hmul2(u32_as_h2(x), u32_as_h2(e | (e << 16))), s2));
+      }
     });
     tc2_tmem_st16(tslot + c * 16, r);
   });
@@ -338,12 +372,8 @@ __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_consta
 
 template <class F>
 tl_status launch_tc2(const Tc2Params& p, const CUtensorMap* tmap, int grid, uint32_t smem_bytes, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(tc2_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
-      return fail(TL_ECUDA, "cudaFuncSetAttribute(tc2 smem)");
-    configured = true;
-  }
+  if (prepare_kernel(reinterpret_cast<const void*>(tc2_kernel<F>), 227 * 1024, kTc2Threads) == 0)
+    return fail(TL_ECUDA, "tc2_kernel: %s", tl_last_error());
   tc2_kernel<F><<<grid, kTc2Threads, smem_bytes, st>>>(*tmap, p);
   return check_launch("tc2_kernel");
 }

@@ -4,31 +4,30 @@
 //
 // Swap-AB tcgen05.mma.cta_group::1.kind::f16: M_mma = 128 weight columns (the dequantized W^T
 // tile, written to TENSOR MEMORY with tcgen05.st -- the "TS" form), N_mma = 16 batch rows (the
-// activation operand, 128B-swizzled K-major in shared memory), fp32 accumulation in TMEM
-// (PAPER.md:191).  The per-weight work is the unpack alone:
+// activation operand, 128B-swizzled K-major in shared memory, rows >= M zero-filled by the TMA
+// unit), fp32 accumulation in TMEM.  The per-weight work is the unpack alone:
 //
-//  * an integer code u placed at bit P of each 16-bit half IS the fp16 u * 2^(P-24) (exact:
-//    fp16 subnormals are multiplied exactly by the tensor core), so the dequant is one AND (plus
-//    one shared SHF per word) per PAIR of weights -- no conversion, no zero-point subtraction;
-//    the activation operand is pre-scaled by 2^-P per k, so the MMA accumulates
-//    D = 2^-24 sum_k A[m,k] u[k,n]; ints are stored offset-binary (zero point 2^(b-1));
-//  * the zero point and the group scale are applied once per (tile, column, batch row) in fp32:
-//        Y[m,n] += s[g,n] * (2^24 * D[n,m] - z[g,n] * sum_{k in tile} A[m,k])
-//    where the activation sums are computed once per tile by the preparation warps;
-//  * float codes are placed on the fp16 exponent/mantissa fields (value * 2^(bias-15), exact)
-//    and Y += s * 2^(15-bias) * D.
+//  * integer codes (layout v2, common.cuh): one LOP3 per pair (more for the few "spare" codes)
+//    places the code at bits [P, P+b) of each half under the fp16 magic 0x6400 (1024 + u*2^P),
+//    and one HFMA2 with the per-tile constant -(2^(10-P) + z) yields u - z EXACTLY in fp16, so the
+//    MMA accumulates D = sum_k A[m,k] (u[k,n] - z) with no further conversion; ints are stored
+//    offset-binary (zero point 2^(b-1));
+//  * float codes are placed on the fp16 sign / exponent / mantissa fields (value * 2^(bias-15),
+//    exact) by the LOP3s alone;
+//  * the group scale is applied once per (tile, column, batch row) in fp32:
+//        Y[m,n] += s[g,n] * D[n,m]      (floats: s[g,n] * 2^(15-bias) * D[n,m]).
 //
-// Everything a tile needs -- the packed weight tile (2048*b B), its scale and zero-point row
-// slices (256 B each) and the M activation row slices (256 B each) -- arrives in ONE TMA ring
-// stage (cp.async.bulk, PAPER.md:148-151 step (1)), so no thread ever waits on a long-latency
-// global load.  Roles (128 + 128*NG threads):
-//   warp 0       TMA producer (one elected thread)
+// The packed weight tile (2048*b B) and its scale and zero-point row slices (256 B each) arrive in
+// ONE TMA ring stage (cp.async.bulk, PAPER.md:148-151 step (1)); the activation operand has its
+// own ring.  Roles (128 + 128*NG threads):
+//   warp 0       weight-stream TMA producer (one elected thread)
 //   warp 1       TMEM allocator + MMA issuer (one elected thread)
-//   warps 2..3   preparation: per stage, sum_k A per row and the pre-scaled swizzled operand
+//   warp 2       activation-operand TMA producer (one elected thread; 2-D tensor map)
+//   warp 3       idle (keeps the dequant warps aligned to TMEM lane quarters)
 //   warps 4..    NG dequant groups of 4 warps (warp%4 = TMEM lane quarter = 32 columns); group
 //                g handles tiles t = g, g+NG, ... of the CTA's stream-K range: unpack into its
-//                W^T slot, hand it to the MMA, then -- one group-iteration late, so it never waits
-//                for its own MMA -- read the tile's accumulator and apply the fp32 fixup.
+//                W^T slot, hand it to the MMA, then -- kTcdLag group-iterations late, so it never
+//                waits for its own MMA -- read the tile's accumulator and apply the fp32 fixup.
 // Stream-K: the linear unit space u = nt*KT + kt is cut into `grid` contiguous
 // ranges; n-tiles shared by several CTAs are reduced in fixed CTA order (reading R12).
 #pragma once
@@ -44,9 +43,8 @@ struct TcdParams {
   int M, N, K, G;
   int units;
   int ns;                          // TMA ring stages
-  uint32_t stage_bytes;            // [weight tile | scale 256 | zero 256 | A M*256 | sums 64]
-  uint32_t w_off, s_off, z_off, a_off;
-  uint32_t sums_off;  // [K/128][MT] fp32: sum_k A[m,k] over every 128-k tile (ints only)
+  uint32_t stage_bytes;            // [weight tile | scale 256 | zero 256]
+  uint32_t w_off, s_off, z_off;
   uint32_t op_off, red_off, bar_off;  // operand ring [kTcdNOP][4 KB] (1024-aligned), reduction, barriers
   const uint8_t* wt;
   const __half* A;
@@ -58,8 +56,11 @@ struct TcdParams {
   float* partial;  // [grid][2][16][128] fp32
   int* sem;
   long long* trace;  // optional [grid][16] %globaltimer stamps (TL_TRACE)
+  uint32_t magic;  // 0x64006400, a kernel argument so that AND-mask + OR-magic fuse into ONE LOP3
+                   // (LOP3 takes one immediate; the magic must live in a register)
+  int static_w;  // TL_FLAG_STATIC_WEIGHTS: the weight stream may start before griddepcontrol.wait
   int dbg;  // experiment knobs (TL_TCD_DBG; device-side ones only with -DTCD_TRACE): 1 skip MMAs,
-            // 4 skip unpack/STTM, 8 skip scale/zero copies, 128 no PDL (host), 256 skip activation sums
+            // 4 skip unpack/STTM, 8 skip scale/zero copies, 128 no PDL (host)
 };
 
 constexpr int kTcdNG = 4;                       // dequant groups
@@ -77,7 +78,6 @@ constexpr int kTcdNB = 16;                      // MMA N (batch rows, zero-padde
 constexpr uint32_t kTcdOpBytes = kTcdNB * 256;  // 16 rows x 128 k fp16, two 64-k SW128 blocks
 constexpr uint32_t kTcdAccCol = 64 * kTcdNW;
 constexpr int kTcdNOP = 8;                      // activation operand ring slots
-constexpr int kTcdNPREP = 1;                    // preparation warps (alternate tiles)
 
 __device__ __forceinline__ void tcd_sttm_x16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(
@@ -111,28 +111,26 @@ __device__ __forceinline__ uint64_t tcd_sw128_desc(uint32_t saddr) {
   d |= (uint64_t)2 << 61;
   return d;
 }
-__device__ __forceinline__ void sts32(uint32_t a, uint32_t x) {
-  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(x) : "memory");
-}
-__device__ __forceinline__ void sts64(uint32_t a, uint32_t x, uint32_t y) {
-  asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(a), "r"(x), "r"(y) : "memory");
-}
 
-// segment words of column n of a transformed tile in shared memory
+// the 4b words of column n of a transformed tile in shared memory (b 16-byte loads)
 template <int B>
 __device__ __forceinline__ void tcd_load_words(uint32_t wtile, int n, uint32_t* words) {
 #pragma unroll
-  for (int s = 0; s < num_segs(B); ++s) {
-    const int w = seg_width(B, s), base = seg_base(B, s);
-#pragma unroll
-    for (int v = 0; v < w; ++v) {
-      const uint4 x = lds128(wtile + 2048 * base + (v * 128 + n) * 16);
-      words[4 * base + 4 * v + 0] = x.x;
-      words[4 * base + 4 * v + 1] = x.y;
-      words[4 * base + 4 * v + 2] = x.z;
-      words[4 * base + 4 * v + 3] = x.w;
-    }
+  for (int v = 0; v < B; ++v) {
+    const uint4 x = lds128(wtile + (v * 128 + n) * 16);
+    words[4 * v + 0] = x.x;
+    words[4 * v + 1] = x.y;
+    words[4 * v + 2] = x.z;
+    words[4 * v + 3] = x.w;
   }
+}
+
+// is P the field position of some pair of the format's plan (ints)?
+template <class F>
+__host__ __device__ constexpr bool plan_uses_p(int P) {
+  for (int i = 0; i < 32; ++i)
+    if (kPlan<F::kind, F::bits, F::exp>.pr[i].P == P) return true;
+  return false;
 }
 
 // Pipeline tracing (tools/trace_tcd.py, tools/trace_pdl.py): compiled in only with -DTCD_TRACE,
@@ -163,7 +161,7 @@ template <class F, int MT>
 __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_constant__ CUtensorMap tmapA, TcdParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  constexpr bool kInt = F::kind != kFloat;  // integer codes: pre-scaled operand + zero-point term
+  constexpr bool kInt = F::kind != kFloat;  // integer codes: magic form + HFMA2 (u - z)
   constexpr uint32_t WB = tile_bytes(F::bits);
   constexpr int NG = kTcdNG, NACC = kTcdNACC;
   const int NS = p.ns;
@@ -227,45 +225,17 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
   tc_fence_after();
   const uint32_t tmem = *tslot_ptr;
   if (threadIdx.x == 0) tcd_stamp(p, 1);
-  const float* sums = reinterpret_cast<const float*>(smem + p.sums_off);
-  // Programmatic dependent launch: the weight stream (warp 0) depends on nothing the previous
-  // kernel in the stream writes, so it starts right away; every other warp waits for the previous
-  // grid (it may have produced A, or still use Y / the workspace) before touching them.
+  // Programmatic dependent launch: with TL_FLAG_STATIC_WEIGHTS the weight stream (warp 0) depends on
+  // nothing a kernel still running in the stream writes, so it starts right away; otherwise warp 0
+  // too waits for the previous grid (which may have produced the weights / scales: only
+  // griddepcontrol.wait makes its writes visible).  Every other warp waits before it reads A or
+  // touches Y / the workspace.
   if (warp == 0) {
+    if (!p.static_w) asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   } else {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (threadIdx.x == 64) tcd_stamp(p, 11);
-    if constexpr (kInt) {
-      // sum_k A[m, k] of the 128-k tiles this CTA touches (zero-point term): one thread per
-      // (tile, row), its 256 B loaded with 16 independent 16-byte loads (one L2 round trip) and
-      // summed in fp32 by four independent chains
-      float* sums_w = reinterpret_cast<float*>(smem + p.sums_off);
-      const int nk = min(KT, T), kt0 = u0 - (u0 / KT) * KT;
-      const int n_pairs = (TCD_TRACE_ON && (p.dbg & 256)) ? 0 : nk * p.M;
-      for (int i = threadIdx.x - 32; i < n_pairs; i += kTcdThreads - 32) {
-        int kt = kt0 + i / p.M;
-        if (kt >= KT) kt -= KT;
-        const int m = i - (i / p.M) * p.M;
-        const uint4* src = reinterpret_cast<const uint4*>(p.A + m * p.lda + (int64_t)kt * kBK);
-        uint4 v[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = __ldg(src + j);
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const uint32_t w4[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 f = __half22float2(u32_as_h2(w4[e]));
-            acc[e] += f.x;
-            acc[e] += f.y;
-          }
-        }
-        sums_w[kt * MT + m] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-      }
-    }
-    named_bar_sync(2, kTcdThreads - 32);  // sums visible to the dequant groups
   }
 
   if (warp == 0 || warp == 2) {
@@ -381,7 +351,7 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     int wsl = g;          // W^T slot of the current tile (t % NW) and its lap (t / NW)
     uint32_t lapw = 0;
-    const float c1mul = kInt ? 16777216.f : (float)(1 << (15 - F::bias));
+    const float c1mul = kInt ? 1.f : (float)(1 << (15 - F::bias));
     float tot[MT];
 #pragma unroll
     for (int m = 0; m < MT; ++m) tot[m] = 0.f;
@@ -430,13 +400,18 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
         uint32_t words[4 * F::bits];
         tcd_load_words<F::bits>(st + p.w_off, n, words);
         const float sc = __half2float(__ushort_as_half(lds16(st + p.s_off + 2 * n)));
+        // ints: -z as fp16x2 (zero point of the tile's group; offset-binary ints: 2^(b-1))
+        uint32_t zneg = 0;
         if constexpr (kInt) {
-          float z = (float)(1 << (F::bits - 1));
-          if constexpr (F::kind == kUint) z = has_zeros ? __half2float(__ushort_as_half(lds16(st + p.z_off + 2 * n))) : 0.f;
-          const float c2 = -sc * z;
-          const float* sa = sums + (u0 + t - nt * KT) * MT;
-#pragma unroll
-          for (int m = 0; m < MT; ++m) tot[m] = fmaf(c2, sa[m], tot[m]);
+          if constexpr (F::kind == kUint) {
+            if (has_zeros) {
+              const uint32_t zb = (uint32_t)lds16(st + p.z_off + 2 * n) ^ 0x8000u;
+              zneg = zb | (zb << 16);
+            }
+          } else {
+            constexpr uint32_t zb = 0x8000u | ((uint32_t)(F::bits - 1 + 15) << 10);  // -2^(b-1)
+            zneg = zb | (zb << 16);
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_tma[s]);
@@ -444,16 +419,37 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
         if (t >= kTcdNW) mbar_wait(&full_acc[(t - kTcdNW) % NACC], (uint32_t)((t - kTcdNW) / NACC) & 1);
         const uint32_t tslot = tmem + lane_off + wsl * 64;
         tcd_istamp(p, dw, lane, kk, 3);
-        if (!(TCD_TRACE_ON && (p.dbg & 4))) static_for<0, 4>([&](auto CC) {
-          constexpr int c = decltype(CC)::value;
-          uint32_t r[16];
-          static_for<0, 16>([&](auto II) {
-            constexpr int ii = decltype(II)::value;
-            if constexpr (kInt) r[ii] = assemble_pair<F::bits, c * 16 + ii, 0>(words);  // u * 2^-24
-            else r[ii] = raw_pair_bits<F, c * 16 + ii>(words);
+        if (!(TCD_TRACE_ON && (p.dbg & 4))) {
+          // per-P constants -(2^(10-P) + z) (exact: integers below 2048)
+          uint32_t cp[10];
+          static_for<0, 10>([&](auto PP) {
+            constexpr int P = decltype(PP)::value;
+            if constexpr (kInt && plan_uses_p<F>(P)) {
+              constexpr uint32_t k = 0x8000u | ((uint32_t)(25 - P) << 10);  // fp16 -2^(10-P)
+              cp[P] = h2_as_u32(__hadd2(u32_as_h2(zneg), u32_as_h2(k | (k << 16))));
+            }
           });
-          tcd_sttm_x16(tslot + c * 16, r);
-        });
+          static_for<0, 4>([&](auto CC) {
+            constexpr int c = decltype(CC)::value;  // pairs 16c .. 16c+15 = TMEM columns of MMAs 2c, 2c+1
+            constexpr int h = c >> 1;                // block
+            uint32_t bw[2 * F::bits];
+#pragma unroll
+            for (int j = 0; j < 2 * F::bits; ++j) bw[j] = words[tile_word(h, j)];
+            uint32_t r[16];
+            static_for<0, 16>([&](auto II) {
+              constexpr int i = (c & 1) * 16 + decltype(II)::value;  // pair within the block
+              if constexpr (kInt) {
+                constexpr int P = kPlan<F::kind, F::bits, F::exp>.pr[i].P;
+                const uint32_t x = extract_pair<F, i>(bw, p.magic);
+                r[decltype(II)::value] =
+                    h2_as_u32(__hfma2(u32_as_h2(x), u32_as_h2(h2_pow2_neg<P>()), u32_as_h2(cp[P])));
+              } else {
+                r[decltype(II)::value] = extract_pair<F, i>(bw, 0u);
+              }
+            });
+            tcd_sttm_x16(tslot + c * 16, r);
+          });
+        }
         tcd_istamp(p, dw, lane, kk, 4);
         tmem_st_wait();
         tcd_istamp(p, dw, lane, kk, 5);
@@ -544,13 +540,8 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
 
 template <class F, int MT>
 tl_status launch_tcd_mt(const TcdParams& p, const CUtensorMap* tmap, int grid, uint32_t smem_bytes, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(tcd_kernel<F, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
-        cudaSuccess)
-      return fail(TL_ECUDA, "cudaFuncSetAttribute(tcd smem)");
-    configured = true;
-  }
+  if (prepare_kernel(reinterpret_cast<const void*>(tcd_kernel<F, MT>), 227 * 1024, kTcdThreads) == 0)
+    return fail(TL_ECUDA, "tcd_kernel: %s", tl_last_error());
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kTcdThreads);

@@ -53,7 +53,7 @@ def test_bad_arguments_rejected_before_any_launch(lib):
     w = lib.wtype("u4")
     # descriptors that are not kernel formats
     for bad in [lib.tl_wtype(0, 9, 0, 0), lib.tl_wtype(2, 8, 5, 2), lib.tl_wtype(2, 6, 3, 3), lib.tl_wtype(3, 4, 0, 0)]:
-        st = lib._lib._tl_matmul(bad, 1, 128, 128, 128, 16, 128, 16, 16, None, 16, 128, 16, 1 << 20, None)
+        st = lib._lib._tl_matmul(bad, 0, 1, 128, 128, 128, 16, 128, 16, 16, None, 16, 128, 16, 1 << 20, None)
         assert lib._lib._tl_status_str(st).decode() == "TL_EINVAL_DTYPE"
     # shape / group / zeros / alignment / workspace checks
     cases = [
@@ -69,18 +69,30 @@ def test_bad_arguments_rejected_before_any_launch(lib):
     for kw, expect in cases:
         a = dict(M=1, N=128, K=128, G=128, A=16, lda=None, ws=1 << 24)
         a.update(kw)
-        st = lib._lib._tl_matmul(w, a["M"], a["N"], a["K"], a["G"], a["A"] or None,
+        st = lib._lib._tl_matmul(w, 0, a["M"], a["N"], a["K"], a["G"], a["A"] or None,
                                  a["lda"] if a["lda"] is not None else a["K"], 16, 16, None, 16, a["N"], 16,
                                  a["ws"], None)
         assert lib._lib._tl_status_str(st).decode() == expect, (kw, lib._lib._tl_last_error())
-    st = lib._lib._tl_matmul(lib.wtype("i4"), 1, 128, 128, 128, 16, 128, 16, 16, 16, 16, 128, 16, 1 << 24, None)
+    st = lib._lib._tl_matmul(lib.wtype("i4"), 0, 1, 128, 128, 128, 16, 128, 16, 16, 16, 16, 128, 16, 1 << 24, None)
     assert lib._lib._tl_status_str(st).decode() == "TL_EZEROS"
     # M == 0 is a no-op
-    st = lib._lib._tl_matmul(w, 0, 128, 128, 128, 16, 128, 16, 16, None, 16, 128, 16, 1 << 24, None)
+    st = lib._lib._tl_matmul(w, 0, 0, 128, 128, 128, 16, 128, 16, 16, None, 16, 128, 16, 1 << 24, None)
     assert st == 0
-    st = lib._lib._tl_matmul(w, 1, 128, 128, 128, 16, 128, 16, 16, None, 16, 128, 16, 64, None)
+    st = lib._lib._tl_matmul(w, 0, 1, 128, 128, 128, 16, 128, 16, 16, None, 16, 128, 16, 64, None)
     assert lib._lib._tl_status_str(st).decode() == "TL_EWORKSPACE"
     assert "workspace" in lib._lib._tl_last_error().decode()
+    # bf16 activations are reserved: rejected, and no workspace size is defined
+    st = lib._lib._tl_matmul(w, 1, 1, 128, 128, 128, 16, 128, 16, 16, None, 16, 128, 16, 1 << 24, None)
+    assert lib._lib._tl_status_str(st).decode() == "TL_EUNSUPPORTED"
+    assert lib.tl_matmul_workspace_bytes(w, 1, 128, 128, 128, atype=lib.TL_ACT_BF16) == 0
+    # tl_matmul_ex: unknown flags / paths, negative splits
+    def ex(path=0, splits=0, flags=0):
+        return lib._lib._tl_status_str(lib._lib._tl_matmul_ex(w, 0, 1, 128, 128, 128, 16, 128, 16, 16, None, 16,
+                                                              128, 16, 1 << 24, path, splits, flags,
+                                                              None)).decode()
+    assert ex(flags=2) == "TL_EINVAL_SHAPE"
+    assert ex(path=7) == "TL_EUNSUPPORTED"
+    assert ex(splits=-1) == "TL_EINVAL_SHAPE"
     del torch
 
 

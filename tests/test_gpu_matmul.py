@@ -13,7 +13,7 @@ from oracle import all_kernel_formats, dequant, matmul_cols_fp64, matmul_fp64, p
 
 pytestmark = pytest.mark.gpu
 FORMATS = [f.name for f in all_kernel_formats()]
-PATHS = {"gemv": 1, "tc": 2, "tcs": 3}
+PATHS = {"gemv": 1, "tc": 2, "tcd": 3}
 
 
 @pytest.fixture(scope="module")
