@@ -185,6 +185,8 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+        if args.gpus != world:
+            raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     G = 128
     M = args.M
     layers = {k: wl.LLAMA33_70B[k] for k in args.layers}
@@ -375,6 +377,9 @@ def run_ours(args):
                "d2h_bytes_per_step": sum(2 * M * p["N"] for p in probs),
                "ms_per_step": round(ems / args.steps, 4)}
 
+    # ---- C5 (BASELINE configs[4]): Llama-3.3-70B gate_up strong-scaled over the ranks ----
+    c5 = None if args.no_c5 else run_c5(args, P, torch, dist, world, rank, dev, peaks)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -393,12 +398,86 @@ def run_ours(args):
             "clocks": sampler.summary(),
             "details": details,
             "details_extra_M": extra,
+            "details_c5": c5,
         }
         if world == 1 and not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline(args.formats, layers, G, M)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_c5(args, P, torch, dist, world, rank, dev, peaks):
+    """gate_up (K=8192, N=57344) column-sharded over the `world` ranks
+    (strong scaling: rank r owns columns column_shard(N, world, r), 57344/P of them), uint4 with
+    zeros and int6, M in {1, 16, 128}.  `sharded_us`: the max over ranks of the device time of the
+    rank's tl_matmul (no communication); `gathered_us`: tl_matmul followed by
+    the NCCL all-gather of the Y shards into Y[M, N] (north star (5)), same timing.  With one rank
+    the gathered variant is the plain matmul."""
+    from paper_2504_12984_b200.dist import column_shard, gather_columns
+    K, N = wl.LLAMA33_70B["gate_up"]
+    G = 128
+    n0, n1 = column_shard(N, world, rank)
+    Ns = n1 - n0
+    out = []
+    reps = 20
+    for fmt in ("u4", "i6"):
+        w = P.wtype(fmt)
+        seed = wl.stable_seed("c5", fmt, rank)
+        codes = wl.gen_codes_torch(fmt, K, Ns, seed, dev)
+        wt = P.tl_transform_weights(w, K, Ns, P.tl_pack(w, K, Ns, codes))
+        del codes
+        s = wl.gen_scales_torch(fmt, K, Ns, G, seed, dev)
+        z = wl.gen_zeros_torch(fmt, K, Ns, G, seed, dev)
+        ws = torch.zeros(P.tl_matmul_workspace_bytes(w, 128, Ns, K, G), dtype=torch.uint8, device=dev)
+        for M in (1, 16, 128):
+            A = wl.gen_activations_torch(M, K, wl.stable_seed("c5A", M), dev)
+            Y = torch.empty((M, Ns), dtype=torch.float16, device=dev)
+            res = {}
+            for variant in ("sharded", "gathered"):
+                def once():
+                    P.tl_matmul_ex(w, M, Ns, K, G, A, wt, s, z, Y, ws, flags=P.TL_FLAG_STATIC_WEIGHTS)
+                    if variant == "gathered" and world > 1:
+                        gather_columns(Y, N, world)
+                for _ in range(3):
+                    once()
+                torch.cuda.synchronize()
+                if world > 1:
+                    dist.barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(reps):
+                    once()
+                e1.record()
+                torch.cuda.synchronize()
+                us = e0.elapsed_time(e1) / reps * 1e3
+                if world > 1:
+                    t = torch.tensor([us], device=dev, dtype=torch.float64)
+                    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                    us = float(t.item())
+                res[variant] = us
+            byts = alg_bytes(fmt, M, K, N, G)
+            out.append({"fmt": fmt, "M": M, "P": world, "shard_cols": Ns, "sharded_us": round(res["sharded"], 2),
+                        "gathered_us": round(res["gathered"], 2),
+                        "GBps_total": round(byts / (res["sharded"] * 1e-6) / 1e9, 1),
+                        "hbm_frac_per_gpu": round(byts / world / (res["sharded"] * 1e-6) / 1e9 / peaks["hbm_gbs"], 3),
+                        "TFLOPs_total": round(2 * M * K * N / (res["sharded"] * 1e-6) / 1e12, 2)})
+        del wt, s, z, ws
+    return out
+
+
+def torchrun_argv(n: int, argv: list[str], port: int) -> list[str]:
+    """The command that relaunches this script with one process per GPU (the driver's own launch
+    form: torch.distributed.run, one node, rendezvous on 127.0.0.1)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + argv
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
 
 
 class _Null:
@@ -422,7 +501,12 @@ def main():
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c5", action="store_true", help="skip the strong-scaled gate_up (configs[4]) block")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N`: start the N ranks ourselves (one process per GPU, NCCL)
+        import subprocess
+        sys.exit(subprocess.call(torchrun_argv(args.gpus, sys.argv[1:], _free_port())))
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

@@ -89,6 +89,16 @@ __device__ __forceinline__ void tma_bulk_g2s_nohint(void* dst, const void* src, 
                : "memory");
 }
 
+// ---- cp.async (LDGSTS): small global -> shared copies tracked by an mbarrier ----------------
+__device__ __forceinline__ void cp_async_8(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+// arrive on `bar` once every cp.async this thread issued so far has landed (the arrival counts
+// against the barrier's expected count: .noinc)
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // ---- TMA: 2-D tensor copy global -> shared ----------------------------------------------
 __device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int32_t c0, int32_t c1, uint64_t* bar,
                                             uint64_t policy) {

@@ -63,24 +63,28 @@ tl_status tcd_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, con
   int grid = grid_req > 0 ? grid_req : sms;
   if (grid > 160) grid = 160;
   if (grid > p.units) grid = p.units;
+  // decode (M = 1) with the activation row resident in shared memory (TcdCfg<1>): K*2 <= 64 KB
+  p.rot = (M <= 1 && K * 2 <= 65536) ? 1 : 0;
   const uint32_t wb = (uint32_t)tile_bytes(w.bits);
-  p.w_off = 0;
-  p.s_off = p.w_off + wb;
-  p.z_off = p.s_off + 256;
-  p.stage_bytes = (p.z_off + 256 + 127) & ~127u;
+  const int R = tcd_tiles_per_stage(w.bits);
+  p.R = R;
+  p.stage_bytes = ((uint32_t)R * (wb + 512) + 127) & ~127u;  // R weight tiles | R scale rows | R zero rows
   const uint32_t red = (uint32_t)kTcdNG * (uint32_t)M * kBN * 4;
-  const uint32_t opb = kTcdNOP * kTcdOpBytes;
-  const uint64_t fixed = 1024 /*align*/ + (uint64_t)opb + 1024 + red + 1024 /*barriers, tmem slot, flags*/;
-  if (fixed + (uint64_t)kTcdNOP * p.stage_bytes > 227u * 1024u)
+  const uint32_t opb = kTcdMaxNOP * kTcdOpBytes;
+  const uint32_t stash = p.rot ? (uint32_t)(K * 2) : 0u;
+  const uint64_t fixed = 1024 /*align*/ + (uint64_t)opb + stash + red + 2048 /*barriers, tmem slot, flags*/;
+  if (fixed + 3ull * p.stage_bytes > 227u * 1024u)
     return TL_ENOFIT;  // caller falls back to the batched path
   int ns = (int)((227u * 1024u - fixed) / p.stage_bytes);
   if (ns > 32) ns = 32;
   if (env_dbg("TL_TCD_NS") > 0 && env_dbg("TL_TCD_NS") < ns) ns = env_dbg("TL_TCD_NS");
   p.ns = ns;
   p.op_off = ((uint32_t)ns * p.stage_bytes + 1023) & ~1023u;
-  p.red_off = p.op_off + opb;
+  p.stash_off = p.op_off + opb;
+  p.red_off = p.stash_off + ((stash + 127) & ~127u);
   p.bar_off = (p.red_off + red + 15) & ~15u;
-  const uint32_t smem = p.bar_off + (3 * ns + kTcdNOP + 2 * kTcdNW + 2 * kTcdNACC) * 8 + 32 + 1024;
+  const uint32_t smem =
+      p.bar_off + (2 * ns + 2 * kTcdMaxNOP + 2 * kTcdMaxNW + 2 * kTcdMaxNACC + 1) * 8 + 32 + 1024;
   if (smem > 227 * 1024) return TL_ENOFIT;
   CUtensorMap tmap;
   tl_status s = make_tmap_a(&tmap, A, M, K, lda, kTcdNB);

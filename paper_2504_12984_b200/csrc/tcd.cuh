@@ -26,7 +26,7 @@
 //   warp 3       idle (keeps the dequant warps aligned to TMEM lane quarters)
 //   warps 4..    NG dequant groups of 4 warps (warp%4 = TMEM lane quarter = 32 columns); group
 //                g handles tiles t = g, g+NG, ... of the CTA's stream-K range: unpack into its
-//                W^T slot, hand it to the MMA, then -- kTcdLag group-iterations late, so it never
+//                W^T slot, hand it to the MMA, then -- TcdCfg::Lag group-iterations late, so it never
 //                waits for its own MMA -- read the tile's accumulator and apply the fp32 fixup.
 // Stream-K: the linear unit space u = nt*KT + kt is cut into `grid` contiguous
 // ranges; n-tiles shared by several CTAs are reduced in fixed CTA order (reading R12).
@@ -43,9 +43,11 @@ struct TcdParams {
   int M, N, K, G;
   int units;
   int ns;                          // TMA ring stages
-  uint32_t stage_bytes;            // [weight tile | scale 256 | zero 256]
-  uint32_t w_off, s_off, z_off;
-  uint32_t op_off, red_off, bar_off;  // operand ring [kTcdNOP][4 KB] (1024-aligned), reduction, barriers
+  int R;                           // tiles per stage (consecutive units: one contiguous weight copy)
+  uint32_t stage_bytes;            // [R weight tiles | R scale row slices | R zero row slices]
+  uint32_t stash_off;              // decode: A[0, 0:K] resident in shared memory (K*2 bytes)
+  int rot;                         // 1: decode configuration TcdCfg<1> (M = 1, K*2 <= 64 KB)
+  uint32_t op_off, red_off, bar_off;  // operand ring [NOP][4 KB] (1024-aligned), reduction, barriers
   const uint8_t* wt;
   const __half* A;
   int64_t lda;
@@ -64,20 +66,43 @@ struct TcdParams {
 };
 
 constexpr int kTcdNG = 4;                       // dequant groups
-#ifndef TCD_NW
-#define TCD_NW 5
+// TMEM budget (512 columns) per batch tile MT:
+//  * MT == 16: NW = 5 W^T slots (64 columns each) + 12 accumulators of 16 columns (one per tile in
+//    flight, slot t % 12), fixups lag 2 group iterations (the accumulator of tile t - NACC must be
+//    read by its group before that group arrives for tile t: 4*lag < NACC);
+//  * MT == 1 (decode): the activation row of tile t is placed in operand row t % 16 (TMA box
+//    starting at row -(t % 16); the other rows are zero-filled), so tile t's result lands in
+//    accumulator COLUMN t % 16 and 16 consecutive tiles share one 16-column block: the first MMA of
+//    tile 16e (accumulate = 0) clears block e % 2, the others accumulate.  Two blocks (32 columns)
+//    leave room for NW = 7 W^T slots, so the dequant groups are not throttled by the slot ring.
+//    NACC is then only the ring of "MMA(t) complete" barriers.  The activation row A[0, :] is
+//    resident in shared memory (one bulk copy) and warp 2 WRITES each tile's operand: slot t % 8
+//    gets A[0, kt*128 : kt*128+128] in row t % 16 and the row it held for tile t - 8 zeroed --
+//    256 + 256 bytes of st.shared per tile instead of a 4 KB TMA box (the stream of small TMA
+//    copies, not HBM, was the decode kernel's throughput limit).
+template <int MT>
+struct TcdCfg {
+  static constexpr bool kRot = MT == 1;                  // row rotation (decode)
+#ifndef TCD_NW_ROT
+#define TCD_NW_ROT 5
 #endif
-constexpr int kTcdNW = TCD_NW;                  // W^T TMEM slots (64 columns each), slot = tile % NW
-constexpr int kTcdNACC = (512 - 64 * kTcdNW) / 16; // accumulator slots (16 TMEM columns each): NW*64 + NACC*16 = 512
-// fixups lag this many group iterations; the accumulator of tile t - NACC must be read by its group
-// before that group arrives for tile t: 4*lag < NACC
-constexpr int kTcdLag = kTcdNACC / 4 - 1;
-static_assert(kTcdNACC % 4 == 0 && kTcdLag >= 1 && kTcdLag <= 2, "TMEM split");
+  static constexpr int NW = kRot ? TCD_NW_ROT : 5;       // W^T slots
+  static constexpr int NACC = kRot ? 16 : 12;            // completion barriers (= accumulators if !kRot)
+  static constexpr int Lag = kRot ? 2 : NACC / 4 - 1;    // fixup lag (group iterations)
+  static constexpr uint32_t AccCol = 64 * NW;            // first accumulator column
+  // activation operand ring: slot t % NOP is refilled once MMA(t - NOP) completed, so the
+  // operand of tile t is in flight for NOP tiles (an L2 round trip); NOP <= NACC keeps the
+  // completion-barrier parity unambiguous
+  static constexpr int NOP = 8;
+  static_assert(NOP <= NACC, "operand ring vs completion ring");
+  static_assert(AccCol + (kRot ? 32 : NACC * 16) <= 512, "TMEM split");
+  static_assert(NACC % 4 == 0 && Lag >= 1 && Lag <= 2 && 4 * Lag < NACC, "fixup lag");
+};
+constexpr int kTcdMaxNW = 7, kTcdMaxNACC = 16;  // shared-memory sizing of the barrier arrays
 constexpr int kTcdThreads = 128 + kTcdNG * 128;
 constexpr int kTcdNB = 16;                      // MMA N (batch rows, zero-padded)
 constexpr uint32_t kTcdOpBytes = kTcdNB * 256;  // 16 rows x 128 k fp16, two 64-k SW128 blocks
-constexpr uint32_t kTcdAccCol = 64 * kTcdNW;
-constexpr int kTcdNOP = 8;                      // activation operand ring slots
+constexpr int kTcdMaxNOP = 8;                   // activation operand ring slots (max over configs)
 
 __device__ __forceinline__ void tcd_sttm_x16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(
@@ -157,31 +182,40 @@ __device__ __forceinline__ void tcd_istamp(const TcdParams& p, int dw, int lane,
     p.trace[2400 + kk * 8 + i] = clock64();
 }
 
+// tiles per weight stage: ~12 KB of packed weights per stage (the cp.async.bulk ring streams at
+// full HBM rate only with stages of ~12 KB and more, tools/tma_probe.cu)
+__host__ __device__ constexpr int tcd_tiles_per_stage(int b) { return (6 + b - 1) / b; }
+
 template <class F, int MT>
 __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_constant__ CUtensorMap tmapA, TcdParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr bool kInt = F::kind != kFloat;  // integer codes: magic form + HFMA2 (u - z)
   constexpr uint32_t WB = tile_bytes(F::bits);
-  constexpr int NG = kTcdNG, NACC = kTcdNACC;
+  constexpr int kR = tcd_tiles_per_stage(F::bits);
+  using Cfg = TcdCfg<MT>;
+  constexpr int NG = kTcdNG, NACC = Cfg::NACC, kTcdNW = Cfg::NW;
+  constexpr uint32_t kTcdAccCol = Cfg::AccCol;
+  constexpr int kTcdNOP = Cfg::NOP;
   const int NS = p.ns;
   const uint32_t SB = p.stage_bytes;
   const uint32_t st_u = smem_u32(smem);
   float* red = reinterpret_cast<float*>(smem + p.red_off);  // [NG][M][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bar_off);
-  uint64_t* full_tma = bars;               // [NS] stage landed
-  uint64_t* full_op = bars + NS;           // [NOP] activation operand landed (NS >= NOP)
-  uint64_t* empty_tma = bars + 2 * NS;     // [NS] group read the stage
-  uint64_t* empty_op = bars + 3 * NS;      // [NOP] MMA done with the operand slot
-  uint64_t* full_w = empty_op + kTcdNOP;   // [NW] W^T slot written
-  uint64_t* empty_w = full_w + kTcdNW;     // [NW] MMA done with the W^T slot
+  uint64_t* full_tma = bars;                    // [NS] stage landed
+  uint64_t* empty_tma = bars + NS;              // [NS] group read the stage
+  uint64_t* full_op = bars + 2 * NS;            // [NOP] activation operand landed
+  uint64_t* empty_op = full_op + kTcdMaxNOP;    // [NOP] (unused: the operand slot is freed by MMA completion)
+  uint64_t* full_w = empty_op + kTcdMaxNOP;  // [NW] W^T slot written
+  uint64_t* empty_w = full_w + kTcdMaxNW;  // [NW] MMA done with the W^T slot
   // [NACC] "MMA(t) complete" (one tcgen05.commit per tile, slot t % NACC).  It also frees the W^T
   // slot and the operand slot of tile t.  No accumulator-empty barrier is needed: the fixup of
   // tile t - NACC is done by the same group (NACC % NG == 0) before it arrives on full_w for t.
   // Every waiter for MMA(j) provably waits before MMA(j + NACC) can complete (parity is safe).
-  uint64_t* full_acc = empty_w + kTcdNW;
-  uint64_t* empty_acc = full_acc + NACC;   // [NACC] accumulator read back
-  uint32_t* tslot_ptr = reinterpret_cast<uint32_t*>(empty_acc + NACC);
+  uint64_t* full_acc = empty_w + kTcdMaxNW;
+  uint64_t* empty_acc = full_acc + kTcdMaxNACC;  // [NACC] accumulator read back
+  uint64_t* stash_bar = empty_acc + kTcdMaxNACC; // decode: A[0, :] landed in the stash
+  uint32_t* tslot_ptr = reinterpret_cast<uint32_t*>(stash_bar + 1);
   int* flag = reinterpret_cast<int*>(tslot_ptr + 4);
 
   const int KT = p.K / kBK;
@@ -198,9 +232,10 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
     tcd_stamp(p, 0);
     if (TCD_TRACE_ON && p.trace) p.trace[blockIdx.x * 16 + 10] = T;
     for (int s = 0; s < NS; ++s) {
-      mbar_init(&full_tma[s], 1);
-      mbar_init(&empty_tma[s], 4);
+      mbar_init(&full_tma[s], 1 + 32);   // the weight TMA (arrive + tx) and warp 3's 32 cp.async lanes
+      mbar_init(&empty_tma[s], 4 * kR);  // every tile of the stage: its group's 4 warps
     }
+    mbar_init(stash_bar, 1);
     for (int i = 0; i < kTcdNOP; ++i) {
       mbar_init(&empty_op[i], 1);
       mbar_init(&full_op[i], 1);
@@ -219,6 +254,12 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
     tmem_alloc(tslot_ptr, 512);
     tmem_relinquish();
   }
+  if constexpr (Cfg::kRot) {
+    // decode: every operand row starts at zero; the writer only ever touches one row per tile
+    uint4* z = reinterpret_cast<uint4*>(smem + p.op_off);
+    for (int i = threadIdx.x; i < kTcdNOP * (int)kTcdOpBytes / 16; i += kTcdThreads) z[i] = make_uint4(0u, 0u, 0u, 0u);
+    fence_proxy_async_smem();
+  }
   const uint32_t op_u = st_u + p.op_off;
   tc_fence_before();
   __syncthreads();
@@ -233,6 +274,8 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
   if (warp == 0) {
     if (!p.static_w) asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  } else if (warp == 3) {
+    if (!p.static_w) asm volatile("griddepcontrol.wait;" ::: "memory");  // scales / zeros
   } else {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (threadIdx.x == 64) tcd_stamp(p, 11);
@@ -250,46 +293,34 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
       const uint64_t pol_last = policy_evict_last();
       int nt = u0 / KT, kt = u0 - (u0 / KT) * KT;
       if (warp == 0) {
-        const bool side = !(TCD_TRACE_ON && (p.dbg & 8));
-        const uint32_t bytes = WB + (side ? 256u + (has_zeros ? 256u : 0u) : 0u);
+        // stage q = tiles [q*R, q*R + R) of the CTA's range: ONE bulk copy of their contiguous
+        // packed bytes (consecutive units are adjacent in the n-tile-major layout).  Large stages:
+        // the streaming rate of cp.async.bulk rings grows with the bytes per stage (measured,
+        // tools/tma_probe.cu), so small-b tiles are grouped.  Scales / zero points are not in the
+        // stage: the dequant threads load their own (2 bytes each), 16 tiles ahead.
         const uint32_t bar0 = smem_u32(full_tma);
         const uint8_t* src = p.wt + (int64_t)u0 * WB;
-        const int tpg = p.G / kBK;  // k-tiles per group
-        int grow = kt / tpg, grem = kt - (kt / tpg) * tpg;
         int s = 0;
         uint32_t ph = 0;
-        for (int t = 0; t < T; ++t) {
-          if (t >= NS) mbar_wait(&empty_tma[s], ph ^ 1);
-          if (t < 64) tcd_tstamp(p, 2720 + t);
+        constexpr int R = kR;
+        for (int t0 = 0, q = 0; t0 < T; t0 += R, ++q) {
+          const int n_t = min(R, T - t0);
+          if (q >= NS) mbar_wait_sleepy(&empty_tma[s], ph ^ 1);
+          if (t0 < 64) tcd_tstamp(p, 2720 + t0);
           const uint32_t st = st_u + s * SB, bar = bar0 + 8 * s;
-          mbar_arrive_expect_tx_u32(bar, bytes);
-          tma_bulk_g2s_cta(st + p.w_off, src, WB, bar, pol_first);
-          if (side) {
-            const int64_t so = (int64_t)grow * p.N + (int64_t)nt * kBN;
-            tma_bulk_g2s_cta(st + p.s_off, p.scales + so, 256, bar, pol_first);
-            if (has_zeros) tma_bulk_g2s_cta(st + p.z_off, p.zeros + so, 256, bar, pol_first);
-          }
-          if (t == 0) tcd_stamp(p, 2);
-          if (t == T - 1) tcd_stamp(p, 3);
-          src += WB;
-          if (++kt == KT) {
-            kt = 0;
-            ++nt;
-            grow = 0;
-            grem = 0;
-          } else if (++grem == tpg) {
-            grem = 0;
-            ++grow;
-          }
+          mbar_arrive_expect_tx_u32(bar, (uint32_t)n_t * WB);
+          tma_bulk_g2s_cta(st, src, (uint32_t)n_t * WB, bar, pol_first);
+          if (t0 == 0) tcd_stamp(p, 2);
+          if (t0 + n_t == T) tcd_stamp(p, 3);
+          src += (int64_t)n_t * WB;
           if (++s == NS) {
             s = 0;
             ph ^= 1;
           }
         }
-      } else {
+      } else if constexpr (!Cfg::kRot) {
         prefetch_tmap(&tmapA);
         int o = 0;
-        uint32_t pho = 0;
         for (int t = 0; t < T; ++t) {
           // operand slot t % NOP is free once MMA(t - NOP) completed (mma_done slot (t - NOP) % NACC)
           if (t >= kTcdNOP) mbar_wait(&full_acc[(t - kTcdNOP) % NACC], (uint32_t)((t - kTcdNOP) / NACC) & 1);
@@ -298,10 +329,37 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
           tma_load_2d(opp, &tmapA, kt * kBK, 0, &full_op[o], pol_last);
           tma_load_2d(opp + kTcdNB * 128, &tmapA, kt * kBK + 64, 0, &full_op[o], pol_last);
           if (++kt == KT) kt = 0;
-          if (++o == kTcdNOP) {
-            o = 0;
-            pho ^= 1;
-          }
+          if (++o == kTcdNOP) o = 0;
+        }
+      }
+    }
+    if constexpr (Cfg::kRot) {
+      if (warp == 2) {
+        // ---- decode operand writer (whole warp): A[0, :] arrived in the stash (prologue); slot
+        // o = t % 8 gets A[0, kt*128 .. +128) in row r = t % 16 (128B-swizzled K-major: two 64-k
+        // blocks of 16 rows x 128 B; 16-byte chunk c of row r at chunk c ^ (r % 8)) and the row it
+        // held for tile t - 8, (r + 8) % 16, zeroed.  Lane l moves k = 4l .. 4l+3.
+        if (lane == 0) {  // after griddepcontrol.wait: A is the previous grid's output
+          mbar_arrive_expect_tx(stash_bar, (uint32_t)p.K * 2u);
+          tma_bulk_g2s(smem + p.stash_off, p.A, (uint32_t)p.K * 2u, stash_bar, policy_evict_last());
+        }
+        mbar_wait(stash_bar, 0);
+        const uint8_t* stash = smem + p.stash_off;
+        const int kb = lane >> 4, c = (lane & 15) >> 1, half = lane & 1;
+        int kt = u0 - (u0 / KT) * KT;
+        int o = 0;
+        for (int t = 0; t < T; ++t) {
+          if (t >= kTcdNOP) mbar_wait(&full_acc[(t - kTcdNOP) % NACC], (uint32_t)((t - kTcdNOP) / NACC) & 1);
+          const uint2 v = *reinterpret_cast<const uint2*>(stash + kt * 256 + lane * 8);
+          const int r = t & 15, rz = (t + 8) & 15;
+          uint8_t* slot = smem + p.op_off + o * kTcdOpBytes + kb * (kTcdNB * 128);
+          *reinterpret_cast<uint2*>(slot + r * 128 + ((c ^ (r & 7)) << 4) + half * 8) = v;
+          *reinterpret_cast<uint2*>(slot + rz * 128 + ((c ^ (rz & 7)) << 4) + half * 8) = make_uint2(0u, 0u);
+          fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core (async proxy)
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full_op[o]);
+          if (++kt == KT) kt = 0;
+          if (++o == kTcdNOP) o = 0;
         }
       }
     }
@@ -319,13 +377,16 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
         if (t < 64) tcd_tstamp(p, 2977 + 3 * t);
         tc_fence_after();
         const uint64_t bd = tcd_sw128_desc(op_u + o * kTcdOpBytes);
-        const uint32_t d = tmem + kTcdAccCol + a * kTcdNB;
+        // accumulator: decode -> block (t / 16) % 2, cleared by the first MMA of tile 16e only;
+        // otherwise accumulator t % NACC, cleared by the tile's first MMA
+        const uint32_t d = Cfg::kRot ? tmem + kTcdAccCol + ((t >> 4) & 1) * kTcdNB : tmem + kTcdAccCol + a * kTcdNB;
+        const uint32_t first = Cfg::kRot ? ((t & 15) == 0 ? 0u : 1u) : 0u;
         const uint32_t aw = tmem + g * 64;
         if (!(TCD_TRACE_ON && (p.dbg & 1)))
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           tcd_mma_ts(d, aw + j * 8, bd + (uint64_t)((j >> 2) * (kTcdNB * 128 / 16) + (j & 3) * 2), idesc,
-                     j > 0 ? 1u : 0u);
+                     j > 0 ? 1u : first);
         tc_commit(&full_acc[a]);  // "MMA(t) complete": frees W^T slot t%NW, operand slot t%NOP, fills acc t%NACC
         if (t < 64) tcd_tstamp(p, 2978 + 3 * t);
         if (t == T - 1) tcd_stamp(p, 8);
@@ -341,7 +402,40 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
       }
     }
   } else if (warp == 3) {
-    // spare warp (keeps the dequant warps aligned to TMEM lane quarters)
+    // ---- scale / zero stager: tile t's row slices s[g, nt*128 : +128] and z[g, ...] (256 B each)
+    // go into the side area of its stage (after the R weight tiles).  Lane l copies columns
+    // 4l .. 4l+3 with 8-byte cp.async (global -> shared, no registers), and after the stage's
+    // last tile each lane arrives on the stage's full barrier when its copies have landed
+    // (cp.async.mbarrier.arrive.noinc), so the stager runs as far ahead as the ring allows.
+    const int tpg = p.G / kBK;
+    int ntf = u0 / KT, ktf = u0 - (u0 / KT) * KT;
+    int growf = ktf / tpg, gremf = ktf - growf * tpg;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int t = 0, j = 0; t < T; ++t) {
+      if (j == 0 && t >= NS * kR) mbar_wait_sleepy(&empty_tma[s], ph ^ 1);
+      const uint32_t side = st_u + s * SB + kR * WB + 256 * j + 8 * lane;
+      const int64_t off = (int64_t)growf * p.N + (int64_t)ntf * kBN + 4 * lane;
+      cp_async_8(side, p.scales + off);
+      if (has_zeros) cp_async_8(side + kR * 256, p.zeros + off);
+      if (++ktf == KT) {
+        ktf = 0;
+        ++ntf;
+        growf = 0;
+        gremf = 0;
+      } else if (++gremf == tpg) {
+        gremf = 0;
+        ++growf;
+      }
+      if (++j == kR || t == T - 1) {
+        cp_async_mbar_arrive_noinc(&full_tma[s]);
+        j = 0;
+        if (++s == NS) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
   } else {
     // ------------------------------ dequant groups ------------------------------
     const int dw = warp - 4;
@@ -360,7 +454,8 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
       const int a = tp % NACC;
       mbar_wait(&full_acc[a], (uint32_t)(tp / NACC) & 1);
       tc_fence_after();
-      const uint32_t ta = tmem + lane_off + kTcdAccCol + a * kTcdNB;
+      const uint32_t ta = Cfg::kRot ? tmem + lane_off + kTcdAccCol + ((tp >> 4) & 1) * kTcdNB + (tp & 15)
+                                    : tmem + lane_off + kTcdAccCol + a * kTcdNB;
       if constexpr (MT == 1) {
         const uint32_t d = tcd_ldtm_x1(ta);
         tmem_ld_wait();
@@ -379,8 +474,9 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
     };
 
     int t = g;
-    int s = g % NS;
-    uint32_t ph = (uint32_t)(g / NS) & 1;
+    int qst = g / kR;  // stage of tile t, its ring slot and phase (tracked incrementally)
+    int s = qst % NS;
+    uint32_t ph = (uint32_t)(qst / NS) & 1;
     uint32_t kk = 0;   // this group's tile counter
     // the fixup of a tile is applied two group-iterations late, so the in-order MMA issuer has
     // reached it by then: tp2 (older) and tp1 are pending, with their scale * c1mul
@@ -396,16 +492,17 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
         mbar_wait(&full_tma[s], ph);
         tcd_istamp(p, dw, lane, kk, 1);
         if (kk == 0 && dw == 0 && lane == 0) tcd_stamp(p, 4);
+        const int jt = t - qst * kR;  // tile within the stage
         const uint32_t st = st_u + s * SB;
         uint32_t words[4 * F::bits];
-        tcd_load_words<F::bits>(st + p.w_off, n, words);
-        const float sc = __half2float(__ushort_as_half(lds16(st + p.s_off + 2 * n)));
+        tcd_load_words<F::bits>(st + jt * WB, n, words);
+        const float sc = __half2float(__ushort_as_half(lds16(st + kR * WB + 256 * jt + 2 * n)));
         // ints: -z as fp16x2 (zero point of the tile's group; offset-binary ints: 2^(b-1))
         uint32_t zneg = 0;
         if constexpr (kInt) {
           if constexpr (F::kind == kUint) {
             if (has_zeros) {
-              const uint32_t zb = (uint32_t)lds16(st + p.z_off + 2 * n) ^ 0x8000u;
+              const uint32_t zb = (uint32_t)lds16(st + kR * WB + kR * 256 + 256 * jt + 2 * n) ^ 0x8000u;
               zneg = zb | (zb << 16);
             }
           } else {
@@ -462,7 +559,7 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
           wsl -= kTcdNW;
           ++lapw;
         }
-        if constexpr (kTcdLag == 2) {
+        if constexpr (Cfg::Lag == 2) {
           if (tp2 >= 0) fixup(tp2, c1p2);
           tp2 = tp1;
           c1p2 = c1p1;
@@ -472,10 +569,14 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
         tcd_istamp(p, dw, lane, kk, 6);
         tp1 = t;
         c1p1 = sc * c1mul;
-        s += NG;
-        while (s >= NS) {
-          s -= NS;
-          ph ^= 1;
+        {
+          const int qn = (t + NG) / kR;
+          s += qn - qst;
+          qst = qn;
+          while (s >= NS) {
+            s -= NS;
+            ph ^= 1;
+          }
         }
       }
       if (dw == 0 && lane == 0) tcd_stamp(p, 5);
@@ -559,8 +660,8 @@ tl_status launch_tcd_mt(const TcdParams& p, const CUtensorMap* tmap, int grid, u
 
 template <class F>
 tl_status launch_tcd(const TcdParams& p, const CUtensorMap* tmap, int grid, uint32_t smem_bytes, cudaStream_t st) {
-  return p.M <= 1 ? launch_tcd_mt<F, 1>(p, tmap, grid, smem_bytes, st)
-                  : launch_tcd_mt<F, kTcdNB>(p, tmap, grid, smem_bytes, st);
+  return p.rot ? launch_tcd_mt<F, 1>(p, tmap, grid, smem_bytes, st)
+               : launch_tcd_mt<F, kTcdNB>(p, tmap, grid, smem_bytes, st);
 }
 
 }  // namespace tl

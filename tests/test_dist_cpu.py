@@ -81,3 +81,17 @@ def test_column_shard_rejects_bad_inputs():
         column_shard(1000, 2, 0)
     with pytest.raises(ValueError):
         column_shard(1024, 2, 2)
+
+
+def test_bench_relaunches_itself_with_one_process_per_gpu():
+    """`python bench.py --gpus N` (no WORLD_SIZE) re-executes under torch.distributed.run with N ranks
+    on 127.0.0.1 and the same arguments (the driver's own launch form)."""
+    import importlib.util
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(root, "bench.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    argv = b.torchrun_argv(4, ["--gpus", "4", "--steps", "7"], 29555)
+    assert argv[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert "--nproc-per-node=4" in argv and "--master-addr=127.0.0.1" in argv and "--master-port=29555" in argv
+    assert argv[-4:] == ["--gpus", "4", "--steps", "7"] and argv[-5].endswith("bench.py")

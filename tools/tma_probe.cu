@@ -62,6 +62,31 @@ __global__ void stream_kernel(const uint8_t* src, size_t bytes_per_cta, int stag
   if (tid == 0) cycles[blockIdx.x] = clock64() - t0;
 }
 
+template <int NS>
+static void run(uint8_t* buf, size_t total, unsigned long long* cyc, int stage, int chunks, int ctas_per_sm,
+                cudaEvent_t e0, cudaEvent_t e1) {
+  const int grid = 148 * ctas_per_sm;
+  size_t per = total / grid;
+  per -= per % stage;
+  const int smem = NS * stage + 2 * NS * 8 + 64;
+  if (smem > 227 * 1024) return;
+  cudaFuncSetAttribute(stream_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  float best = 1e30f;
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaEventRecord(e0);
+    stream_kernel<NS><<<grid, 160, smem>>>(buf, per, stage, chunks, chunks, cyc);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  cudaError_t err = cudaGetLastError();
+  printf("NS=%2d stage=%6d chunks=%d ctas/SM=%d smem=%6d in-flight/SM=%6d : %.1f GB/s %s\n", NS, stage, chunks,
+         ctas_per_sm, smem, NS * stage * ctas_per_sm, (double)per * grid / (best * 1e-3) / 1e9,
+         err == cudaSuccess ? "" : cudaGetErrorString(err));
+}
+
 int main() {
   const size_t total = (size_t)2 << 30;  // 2 GiB
   uint8_t* buf;
@@ -72,28 +97,13 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  struct Cfg { int stage, chunks, issuers, ctas_per_sm; };
-  std::vector<Cfg> cfgs = {{8192, 1, 1, 1}, {8192, 4, 4, 1},   {8192, 8, 8, 1},   {16384, 1, 1, 1},
-                           {16384, 8, 8, 1}, {32768, 1, 1, 1}, {32768, 16, 16, 1}, {8192, 1, 1, 2},
-                           {8192, 1, 1, 4}, {4096, 1, 1, 1},  {2048, 1, 1, 1},   {16384, 1, 1, 2}};
-  for (auto c : cfgs) {
-    const int grid = 148 * c.ctas_per_sm;
-    size_t per = total / grid;
-    per -= per % c.stage;
-    const int NS = 8;
-    const int smem = NS * c.stage + 2 * NS * 8 + 64;
-    cudaFuncSetAttribute(stream_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    for (int rep = 0; rep < 2; ++rep) {
-      cudaEventRecord(e0);
-      stream_kernel<8><<<grid, 160, smem>>>(buf, per, c.stage, c.chunks, c.issuers, cyc);
-      cudaEventRecord(e1);
-      cudaEventSynchronize(e1);
+  for (int stage : {2560, 6656, 12544, 16896, 13312}) {
+    for (int chunks : {1, 2}) {
+      run<8>(buf, total, cyc, stage, chunks, 1, e0, e1);
+      run<16>(buf, total, cyc, stage, chunks, 1, e0, e1);
+      run<24>(buf, total, cyc, stage, chunks, 1, e0, e1);
+      run<32>(buf, total, cyc, stage, chunks, 1, e0, e1);
     }
-    cudaError_t err = cudaGetLastError();
-    float ms = 0;
-    cudaEventElapsedTime(&ms, e0, e1);
-    printf("stage=%6d chunks=%2d issuers=%2d ctas/SM=%d smem=%6d : %.1f GB/s %s\n", c.stage, c.chunks, c.issuers,
-           c.ctas_per_sm, smem, (double)per * grid / (ms * 1e-3) / 1e9, err == cudaSuccess ? "" : cudaGetErrorString(err));
   }
   return 0;
 }

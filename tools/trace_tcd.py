@@ -16,9 +16,10 @@ for _ in range(3):
     flush.zero_()
     P.tl_matmul_ex(w, M, N, K, 128, A, wt, s, z, Y, ws, path=3)
 torch.cuda.synchronize()
-buf = (ctypes.c_longlong * (16 * 256))()
+buf = (ctypes.c_longlong * (2 * 16 * 256))()
 P._lib._lib.tl__debug_trace(buf)
-a = np.array(buf, dtype=np.int64).reshape(256, 16)
+full = np.array(buf, dtype=np.int64)[:16 * 256]  # launch 3 of 3 used trace buffer 0 (they alternate)
+a = full.reshape(256, 16)
 g = int((a[:, 10] > 0).sum())
 a = a[:g]
 t0 = a[:, 0].min()
@@ -29,12 +30,12 @@ for c in list(range(0, g, max(1, g // 12))) + [g - 1]:
 for i, n in enumerate(names[:10]):
     v = (a[:, i] - t0) / 1e3
     print(f"{n:6s} min {v.min():7.2f} med {np.median(v):7.2f} max {v.max():7.2f}")
-it = np.array(buf, dtype=np.int64)[2400:2400 + 40 * 8].reshape(40, 8)
+it = full[2400:2400 + 40 * 8].reshape(40, 8)
 print("group 0 iterations (clock64 deltas): top->prep_ok, ->read_done, ->wslot_free, ->sttm_issued, ->st_done, ->fixup_done, iter_total")
 for k in range(1, 40):
     r = it[k]
     print(f"{k:3d} " + " ".join(f"{r[i + 1] - r[i]:6d}" for i in range(6)) + f" {it[k][0] - it[k - 1][0]:7d}")
-b = np.array(buf, dtype=np.int64)
+b = full
 pr = b[2720:2784]; pp = b[2784:2976].reshape(64, 3); mm = b[2976:3168].reshape(64, 3)
 base = pr[0]
 print("tile  prod_issue | prep: data_ok op_ok done | mma: fullw_ok acc_ok committed   (clock64 from first issue)")
