@@ -112,7 +112,7 @@ size_t tc_workspace_bytes(int64_t M, int64_t N, int64_t K) {
   (void)N;
   (void)K;
   const int nb = round_up((int)(M < 128 ? M : 128), 16);
-  return (size_t)kTcMaxCtas * 2 * nb * 128 * 4;
+  return (size_t)kTcMaxCtas * 2 /*slots*/ * 2 /*n-pair tiles*/ * nb * 128 * 4;
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -159,7 +159,8 @@ tl_status tc_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, cons
     p.K = (int)K;
     p.G = G;
     p.NB = round_up(mc, 16);
-    p.units = (int)((N / kBN) * (K / kBK));
+    p.NT = (int)(N / kBN);
+    p.units = (int)(((N / kBN + 1) / 2) * (K / kBK));  // (n-pair, k-tile) units
     p.wt = wt;
     p.scales = scales;
     p.zeros = zeros;
@@ -168,15 +169,15 @@ tl_status tc_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, cons
     p.partial = partial;
     p.sem = sem;
     p.magic = 0x64006400u;
-    // stage: [activation boxes NB x 256 B (1024-aligned, 128B swizzle) | packed weight tile]
+    // stage: [activation boxes NB x 256 B (1024-aligned, 128B swizzle) | weight tile 2p | weight tile 2p+1]
     const uint32_t wb = (uint32_t)tile_bytes(w.bits);
-    p.a_off_in_stage = (uint32_t)p.NB * 256;
-    p.stage_bytes = (p.a_off_in_stage + wb + 1023) & ~1023u;
+    p.w_off_in_stage = (uint32_t)p.NB * 256;
+    p.stage_bytes = (p.w_off_in_stage + 2 * wb + 1023) & ~1023u;
     const uint32_t budget = 227 * 1024 - 1024 - 512;
     int ns = 16;
     while (ns > 2 && (uint32_t)ns * p.stage_bytes > budget) --ns;
     p.ns = ns;
-    const uint32_t smem = ns * p.stage_bytes + (2 * ns + 2 * kTc2WSlots + 2) * 8 + 32 + 1024;
+    const uint32_t smem = ns * p.stage_bytes + (2 * ns + 2 * kTc2Groups + 2) * 8 + 32 + 1024;
     if (smem > 227 * 1024)
       return fail(TL_EUNSUPPORTED, "tensor-core tile does not fit shared memory (ns=%d stage=%u smem=%u)", ns,
                   p.stage_bytes, smem);

@@ -1,25 +1,27 @@
-// tc2.cuh -- batched tensor-core path (any M, any group): SURVEY §8(a) rows a3-a11, K-B3.
+// tc2.cuh -- batched tensor-core path (M > 16, any group): SURVEY §8(a) rows a3-a11, K-B3.
 //
 // Paper: "Tensor Cores for 16 or more tokens" with software pipelining and stream-K
 // (PAPER.md:546); the weight pipeline of fig:weight-pipeline(c).  B200 form:
 //
-//   D[n 128, m NB] (fp32, TMEM) += W^T[n 128, k 16] (fp16, TMEM) x A^T[k 16, m NB] (fp16, smem)
+//   D_j[n 128, m NB] (fp32, TMEM) += W_j^T[n 128, k 16] (fp16, TMEM) x A^T[k 16, m NB] (fp16, smem)
 //
-// (swap-AB: the weight tile fills the 128 MMA rows, the batch is MMA-N, NB <= 128 per launch).
-//   warp 0      TMA producer: per k-tile one cp.async.bulk of the packed 128x128 weight tile
-//               and two 2-D tensor boxes of the activations (128B swizzle, rows >= M
-//               zero-filled) -> NS-stage ring.
-//   warp 1      TMEM owner + MMA issuer (one thread): 8 x tcgen05.mma.cta_group::1.kind::f16 per
-//               k-tile with the A operand (the dequantized W^T) read from TENSOR MEMORY ("TS"),
-//               accumulating the whole K range of an n-tile in one TMEM accumulator.
-//   warps 2..13 three dequant groups of 4 warps (warp%4 = TMEM lane quarter); group g handles
-//               tiles t = g, g+3, ... into its two TMEM W^T slots (double buffer): LDS of the
-//               column's words, LOP3 (layout v2, common.cuh) + HFMA2 (magic number) -> exact
-//               (u - z) / value(code) fp16 pairs, HMUL2 by the group scale (reading R9),
-//               tcgen05.st.  The same
-//               warps run the epilogue (tcgen05.ld -> fp16 -> Y, or a stream-K partial with a
-//               deterministic fixup) at the end of every 128-column n-tile.
-// Scales / zeros are read by the dequant threads straight from global memory, PF tiles ahead.
+// swap-AB: the weight tile fills the 128 MMA rows, the batch is MMA-N (NB <= 128 per launch).
+// A UNIT is one k-tile of an n-PAIR: the activation tile A[:, kt*128 : +128] (NB x 256 B) is
+// staged once and feeds the MMAs of two 128-column weight tiles (n-tiles 2p and 2p+1), halving
+// the L2 -> SM activation traffic (at NB = 128 and full tensor rate, one activation tile per
+// weight tile would need more L2 bandwidth than the chip has).
+//   warp 0      TMA producer: per unit two 64-k x NB-row boxes of A (128B swizzle, rows >= M
+//               zero-filled) + one cp.async.bulk per weight tile (2048*b B) -> NS-stage ring.
+//   warp 1      TMEM owner + MMA issuer (one thread): 16 x tcgen05.mma.cta_group::1.kind::f16 per
+//               unit, the A operand (the dequantized W^T) read from TENSOR MEMORY ("TS"), the two
+//               accumulators D_0, D_1 hold the CTA's K range of the n-pair.
+//   warps 2..9  two dequant groups of 4 warps (warp%4 = TMEM lane quarter); group g handles the
+//               units t = g, g+2, ... into its W^T slot pair: LDS of the column's words,
+//               LOP3 (layout v2, common.cuh) + HFMA2 (magic number) -> exact (u - z) /
+//               value(code) fp16 pairs, HMUL2 by the group scale (reading R9), tcgen05.st.
+//               At the end of an n-pair both groups run the epilogue (group j: accumulator D_j).
+// TMEM columns: [0,128) W^T slots of group 0 (tile 0 | tile 1), [128,256) group 1,
+// [256,384) D_0, [384,512) D_1.
 #pragma once
 
 #include <cuda.h>
@@ -32,23 +34,23 @@ namespace tl {
 struct Tc2Params {
   int M, N, K, G;
   int NB;          // MMA N = batch tile (multiple of 16, <= 128)
-  int units;
+  int NT;          // n-tiles (N / 128)
+  int units;       // n-pairs * KT
   int ns;          // TMA ring stages
-  uint32_t stage_bytes, a_off_in_stage;
+  uint32_t stage_bytes, w_off_in_stage;  // [A boxes NB*256 | W tile 0 | W tile 1]
   const uint8_t* wt;
   const __half* scales;
   const __half* zeros;
   __half* Y;
   int64_t ldy;
-  float* partial;  // [grid][2][NB][128]
-  int* sem;
-  uint32_t magic;  // 0x64006400
+  float* partial;  // [grid][2 slots][2 tiles][NB][128]
+  int* sem;        // [n-pairs]
+  uint32_t magic;  // 0x64006400 (a kernel argument: the LOP3 takes one immediate, see tcd)
 };
 
-constexpr int kTc2Groups = 3;
+constexpr int kTc2Groups = 2;
 constexpr int kTc2Threads = 64 + kTc2Groups * 128;
-constexpr int kTc2WSlots = 2 * kTc2Groups;          // W^T tiles in TMEM (64 columns each)
-constexpr uint32_t kTc2AccCol = 64 * kTc2WSlots;    // accumulator columns [384, 384 + NB)
+constexpr uint32_t kTc2AccCol = 256;  // D_0 at 256, D_1 at 384
 
 __device__ __forceinline__ void tc2_tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(
@@ -84,14 +86,15 @@ __host__ __device__ constexpr bool tc2_plan_uses_p(int P) {
   return false;
 }
 
-// Dequantize row n of one tile (64 pairs, layout v2) into a TMEM W^T slot; scales / zeros of the
-// tile's (up to four) 32-k sub-pieces come in sc[4] / zc[4] (fp16 bits).
+// Dequantize column n of one weight tile (64 pairs, layout v2) into the 64 TMEM columns at
+// tslot.  sc[c] / zc[c]: fp16 bits of the scale / zero of 32-k sub-piece c (all four equal when
+// the group size is a multiple of 128).
 //   ints:   LOP3(s) -> 1024 + u*2^P (magic form); HFMA2(x, 2^-P, -(2^(10-P) + z)) = u - z exactly;
 //           HMUL2 by s (one fp16 rounding, reading R9)
 //   floats: LOP3(s) -> value(code) * 2^(bias-15) exactly; HMUL2 by 2^(15-bias) (exact), HMUL2 by s
-template <class F>
+template <class F, bool kSubG>
 __device__ __forceinline__ void tc2_dequant_tile(uint32_t wtile, int n, uint32_t tslot, uint32_t magic,
-                                                 const uint16_t (&sc)[4], const uint16_t (&zc)[4]) {
+                                                 const uint32_t (&sc)[4], const uint32_t (&zc)[4]) {
   constexpr int B = F::bits;
   uint32_t words[4 * B];
 #pragma unroll
@@ -102,18 +105,13 @@ __device__ __forceinline__ void tc2_dequant_tile(uint32_t wtile, int n, uint32_t
     words[4 * v + 2] = x.z;
     words[4 * v + 3] = x.w;
   }
-  static_for<0, 4>([&](auto CC) {
-    constexpr int c = decltype(CC)::value;  // 16 pairs = one 32-k sub-piece = 16 TMEM columns
-    constexpr int h = c >> 1;
-    uint32_t bw[2 * B];
-#pragma unroll
-    for (int j = 0; j < 2 * B; ++j) bw[j] = words[tile_word(h, j)];
-    const __half2 s2 = u32_as_h2((uint32_t)sc[c] | ((uint32_t)sc[c] << 16));
-    uint32_t cp[10];
+  uint32_t cp[kSubG ? 4 : 1][10];
+  static_for<0, (kSubG ? 4 : 1)>([&](auto CC) {
+    constexpr int c = decltype(CC)::value;
     if constexpr (F::kind != kFloat) {
       uint32_t zneg;
       if constexpr (F::kind == kUint) {
-        const uint32_t zb = (uint32_t)zc[c] ^ 0x8000u;
+        const uint32_t zb = zc[c] ^ 0x8000u;
         zneg = zb | (zb << 16);
       } else {
         constexpr uint32_t zb = 0x8000u | ((uint32_t)(B - 1 + 15) << 10);  // -2^(b-1)
@@ -123,10 +121,19 @@ __device__ __forceinline__ void tc2_dequant_tile(uint32_t wtile, int n, uint32_t
         constexpr int P = decltype(PP)::value;
         if constexpr (tc2_plan_uses_p<F>(P)) {
           constexpr uint32_t k = 0x8000u | ((uint32_t)(25 - P) << 10);  // fp16 -2^(10-P)
-          cp[P] = h2_as_u32(__hadd2(u32_as_h2(zneg), u32_as_h2(k | (k << 16))));
+          cp[c][P] = h2_as_u32(__hadd2(u32_as_h2(zneg), u32_as_h2(k | (k << 16))));
         }
       });
     }
+  });
+  static_for<0, 4>([&](auto CC) {
+    constexpr int c = decltype(CC)::value;  // 16 pairs = one 32-k sub-piece = 16 TMEM columns
+    constexpr int cs = kSubG ? c : 0;
+    constexpr int h = c >> 1;
+    uint32_t bw[2 * B];
+#pragma unroll
+    for (int j = 0; j < 2 * B; ++j) bw[j] = words[tile_word(h, j)];
+    const __half2 s2 = u32_as_h2(sc[cs] | (sc[cs] << 16));
     uint32_t r[16];
     static_for<0, 16>([&](auto II) {
       constexpr int ii = decltype(II)::value;
@@ -134,7 +141,7 @@ __device__ __forceinline__ void tc2_dequant_tile(uint32_t wtile, int n, uint32_t
       if constexpr (F::kind != kFloat) {
         constexpr int P = kPlan<F::kind, F::bits, F::exp>.pr[i].P;
         const uint32_t x = extract_pair<F, i>(bw, magic);
-        const __half2 v = __hfma2(u32_as_h2(x), u32_as_h2(h2_pow2_neg<P>()), u32_as_h2(cp[P]));
+        const __half2 v = __hfma2(u32_as_h2(x), u32_as_h2(h2_pow2_neg<P>()), u32_as_h2(cp[cs][P]));
         r[ii] = h2_as_u32(__hmul2(v, s2));
       } else {
         constexpr uint32_t e = (uint32_t)(30 - F::bias) << 10;  // fp16 bits of 2^(15-bias)
@@ -146,22 +153,22 @@ __device__ __forceinline__ void tc2_dequant_tile(uint32_t wtile, int n, uint32_t
   });
 }
 
-template <class F>
+template <class F, bool kSubG>
 __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_constant__ CUtensorMap tmapA, Tc2Params p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr uint32_t WB = tile_bytes(F::bits);
   const int NS = p.ns;
   const int NB = p.NB;
-  const uint32_t stage_bytes = p.stage_bytes;
-  uint8_t* st = smem;  // NS x [activation boxes (1024-aligned) | packed weight tile]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NS * stage_bytes);
+  const uint32_t SB = p.stage_bytes;
+  uint8_t* st = smem;  // NS x [activation boxes (1024-aligned) | weight tile 0 | weight tile 1]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NS * SB);
   uint64_t* full_tma = bars;
-  uint64_t* empty_tma = bars + NS;
-  uint64_t* full_w = bars + 2 * NS;             // [6]
-  uint64_t* empty_w = full_w + kTc2WSlots;      // [6]
-  uint64_t* acc_full = empty_w + kTc2WSlots;    // [1]
-  uint64_t* acc_empty = acc_full + 1;           // [1]
+  uint64_t* empty_tma = bars + NS;                // the group (4 warps) + the MMA commit
+  uint64_t* full_w = bars + 2 * NS;               // [2] group g's W^T slot pair written
+  uint64_t* empty_w = full_w + kTc2Groups;        // [2] MMA done with it
+  uint64_t* acc_full = empty_w + kTc2Groups;      // [1] the n-pair's last MMA completed
+  uint64_t* acc_empty = acc_full + 1;             // [1] the epilogue drained both accumulators
   uint32_t* tslot_ptr = reinterpret_cast<uint32_t*>(acc_empty + 1);
   int* flag = reinterpret_cast<int*>(tslot_ptr + 4);
 
@@ -178,9 +185,9 @@ __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_consta
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full_tma[s], 1);
-      mbar_init(&empty_tma[s], 4 + 1);  // the dequant group (4 warps) + the MMA commit
+      mbar_init(&empty_tma[s], 4 + 1);
     }
-    for (int i = 0; i < kTc2WSlots; ++i) {
+    for (int i = 0; i < kTc2Groups; ++i) {
       mbar_init(&full_w[i], 4);
       mbar_init(&empty_w[i], 1);
     }
@@ -203,16 +210,23 @@ __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_consta
     if (elect_one()) {
       const uint64_t pol_w = policy_evict_first();
       const uint64_t pol_a = policy_evict_last();
-      const uint32_t bytes = WB + (uint32_t)NB * 256;
-      int s = 0, ph = 0, kt = u0 % KT;
+      const uint32_t abytes = (uint32_t)NB * 256;
+      int s = 0, ph = 0;
+      int np = u0 / KT, kt = u0 - (u0 / KT) * KT;
       for (int t = 0; t < T; ++t) {
+        const bool two = 2 * np + 1 < p.NT;
         if (t >= NS) mbar_wait_sleepy(&empty_tma[s], ph ^ 1);
-        uint8_t* sp = st + s * stage_bytes;
-        mbar_arrive_expect_tx(&full_tma[s], bytes);
+        uint8_t* sp = st + s * SB;
+        mbar_arrive_expect_tx(&full_tma[s], abytes + (two ? 2 : 1) * WB);
         tma_load_2d(sp, &tmapA, kt * kBK, 0, &full_tma[s], pol_a);
         tma_load_2d(sp + NB * 128, &tmapA, kt * kBK + 64, 0, &full_tma[s], pol_a);
-        tma_bulk_g2s(sp + p.a_off_in_stage, p.wt + (int64_t)(u0 + t) * WB, WB, &full_tma[s], pol_w);
-        if (++kt == KT) kt = 0;
+        const uint8_t* w0 = p.wt + ((int64_t)(2 * np) * KT + kt) * WB;
+        tma_bulk_g2s(sp + p.w_off_in_stage, w0, WB, &full_tma[s], pol_w);
+        if (two) tma_bulk_g2s(sp + p.w_off_in_stage + WB, w0 + (int64_t)KT * WB, WB, &full_tma[s], pol_w);
+        if (++kt == KT) {
+          kt = 0;
+          ++np;
+        }
         if (++s == NS) { s = 0; ph ^= 1; }
       }
     }
@@ -221,22 +235,26 @@ __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_consta
     if (elect_one()) {
       const uint32_t idesc = (1u << 4) | ((uint32_t)(NB >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
       const uint32_t bblk = (uint32_t)NB * 8;  // NB*128 B in 16-B descriptor units
-      int s = 0, ph = 0, kt = u0 % KT, seg = 0;
+      int s = 0, ph = 0, np = u0 / KT, kt = u0 - (u0 / KT) * KT, seg = 0;
       bool first = true;
       for (int t = 0; t < T; ++t) {
-        const int gk = t / kTc2Groups, gg = t - gk * kTc2Groups;
-        const int ws = 2 * gg + (gk & 1);
-        if (first && seg >= 1) mbar_wait(acc_empty, (seg - 1) & 1);  // epilogue drained the accumulator
-        mbar_wait(&full_w[ws], (gk >> 1) & 1);
-        mbar_wait(&full_tma[s], ph);
+        const int g = t & 1;
+        const bool two = 2 * np + 1 < p.NT;
+        if (first && seg >= 1) mbar_wait(acc_empty, (seg - 1) & 1);  // epilogue drained the accumulators
+        mbar_wait(&full_w[g], (t >> 1) & 1);
         tc_fence_after();
-        const uint64_t bd0 = tc2_sw128_desc(smem_u32(st + s * stage_bytes));
-        const uint32_t aw = tmem + ws * 64;
+        const uint64_t bd0 = tc2_sw128_desc(smem_u32(st + s * SB));
+        const uint32_t aw = tmem + g * 128;
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          tc2_mma_ts(tmem + kTc2AccCol, aw + j * 8, bd0 + (uint64_t)((j >> 2) * bblk + (j & 3) * 2), idesc,
-                     (first && j == 0) ? 0u : 1u);
-        tc_commit(&empty_w[ws]);
+        for (int j = 0; j < 2; ++j) {
+          if (j == 0 || two) {
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks)
+              tc2_mma_ts(tmem + kTc2AccCol + j * 128, aw + j * 64 + ks * 8,
+                         bd0 + (uint64_t)((ks >> 2) * bblk + (ks & 3) * 2), idesc, (first && ks == 0) ? 0u : 1u);
+          }
+        }
+        tc_commit(&empty_w[g]);
         tc_commit(&empty_tma[s]);
         first = false;
         if (kt == KT - 1 || t == T - 1) {
@@ -244,13 +262,16 @@ __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_consta
           first = true;
           ++seg;
         }
-        if (++kt == KT) kt = 0;
+        if (++kt == KT) {
+          kt = 0;
+          ++np;
+        }
         if (++s == NS) { s = 0; ph ^= 1; }
       }
     }
   } else {
     // ------------------------------ dequant groups + epilogue ------------------------------
-    const int dw = warp - 2;            // 0..11
+    const int dw = warp - 2;            // 0..7
     const int g = dw >> 2;              // dequant group
     const int q = warp & 3;             // TMEM lane quarter
     const int n = q * 32 + lane;        // row of W^T = output column within the n-tile
@@ -258,22 +279,28 @@ __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_consta
     const uint32_t st_u = smem_u32(st);
     const unsigned short* sg = reinterpret_cast<const unsigned short*>(p.scales);
     const unsigned short* zg = reinterpret_cast<const unsigned short*>(p.zeros);
-    // scale / zero prefetch (PF group-iterations ahead), group rows tracked from (nt, kt)
+    // scale / zero of this thread's column for both tiles of unit t, PF group-iterations ahead
     constexpr int PF = 2;
+    constexpr int NSC = kSubG ? 4 : 1;
     const int lgG = p.G == 32 ? 5 : (p.G == 64 ? 6 : 0);  // G < 128: row = k >> lgG
     const int tpg = p.G >= kBK ? p.G / kBK : 1;            // G >= 128: k-tiles per group
-    auto fetch = [&](int tt, uint16_t (&sc)[4], uint16_t (&zc)[4]) {
-      const int u = u0 + tt, nt_ = u / KT, kt_ = u - nt_ * KT;
-      const int trow = lgG ? 0 : (tpg == 1 ? kt_ : kt_ / tpg);
+    auto fetch = [&](int tt, uint32_t (&sc)[2][4], uint32_t (&zc)[2][4]) {
+      const int u = u0 + tt, np_ = u / KT, kt_ = u - np_ * KT;
+      const int trow = kSubG ? 0 : (tpg == 1 ? kt_ : kt_ / tpg);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int row = lgG ? ((kt_ * kBK + c * 32) >> lgG) : trow;
-        const int64_t off = (int64_t)row * p.N + nt_ * kBN + n;
-        sc[c] = __ldg(sg + off);
-        zc[c] = (F::kind == kUint && has_zeros) ? __ldg(zg + off) : (unsigned short)0;
+      for (int j = 0; j < 2; ++j) {
+        const int col = (2 * np_ + j) * kBN + n;
+        const bool ok = (2 * np_ + j) < p.NT;
+#pragma unroll
+        for (int c = 0; c < NSC; ++c) {
+          const int row = kSubG ? ((kt_ * kBK + c * 32) >> lgG) : trow;
+          const int64_t off = (int64_t)row * p.N + col;
+          sc[j][c] = ok ? (uint32_t)__ldg(sg + off) : 0u;
+          zc[j][c] = (ok && F::kind == kUint && has_zeros) ? (uint32_t)__ldg(zg + off) : 0u;
+        }
       }
     };
-    uint16_t scq[PF][4], zcq[PF][4];
+    uint32_t scq[PF][2][4], zcq[PF][2][4];
 #pragma unroll
     for (int pf = 0; pf < PF; ++pf)
       if (g + pf * kTc2Groups < T) fetch(g + pf * kTc2Groups, scq[pf], zcq[pf]);
@@ -282,55 +309,65 @@ __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_consta
     int t0 = 0;
     while (t0 < T) {
       const int ufirst = u0 + t0;
-      const int nt = ufirst / KT;
-      const int t1 = min(T, t0 + (KT - (ufirst - nt * KT)));
+      const int np = ufirst / KT;
+      const int t1 = min(T, t0 + (KT - (ufirst - np * KT)));
+      const bool two = 2 * np + 1 < p.NT;
       for (; t < t1; t += kTc2Groups, ++kk) {
-        const int ws = 2 * g + (kk & 1);
-        uint16_t sc[4], zc[4];
+        uint32_t sc[2][4], zc[2][4];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          sc[c] = scq[0][c];
-          zc[c] = zcq[0][c];
-        }
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            sc[j][c] = scq[0][j][c];
+            zc[j][c] = zcq[0][j][c];
+          }
 #pragma unroll
         for (int pf = 0; pf + 1 < PF; ++pf)
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            scq[pf][c] = scq[pf + 1][c];
-            zcq[pf][c] = zcq[pf + 1][c];
-          }
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              scq[pf][j][c] = scq[pf + 1][j][c];
+              zcq[pf][j][c] = zcq[pf + 1][j][c];
+            }
         if (t + PF * kTc2Groups < T) fetch(t + PF * kTc2Groups, scq[PF - 1], zcq[PF - 1]);
         const int s = t % NS;
         mbar_wait(&full_tma[s], (t / NS) & 1);
-        if (kk >= 2) mbar_wait(&empty_w[ws], ((kk >> 1) - 1) & 1);
-        tc2_dequant_tile<F>(st_u + s * stage_bytes + p.a_off_in_stage, n, tmem + lane_off + ws * 64, p.magic, sc, zc);
+        if (kk >= 1) mbar_wait(&empty_w[g], (kk - 1) & 1);  // MMA of this group's previous unit done
+        const uint32_t wst = st_u + s * SB + p.w_off_in_stage;
+        tc2_dequant_tile<F, kSubG>(wst, n, tmem + lane_off + g * 128, p.magic, sc[0], zc[0]);
+        if (two) tc2_dequant_tile<F, kSubG>(wst + WB, n, tmem + lane_off + g * 128 + 64, p.magic, sc[1], zc[1]);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          mbar_arrive(&full_w[ws]);
+          mbar_arrive(&full_w[g]);
           mbar_arrive(&empty_tma[s]);
         }
       }
-      // ---- epilogue of n-tile nt: the accumulator holds this CTA's K range of it ----
+      // ---- epilogue of n-pair np: group j owns accumulator D_j (n-tile 2np + j) ----
       mbar_wait(acc_full, seg & 1);
       tc_fence_after();
-      const int ua = nt * KT, ub = ua + KT;
+      const int nt = 2 * np + g;
+      const int ua = np * KT, ub = ua + KT;
       const bool complete = (u0 <= ua) && (u1 >= ub);
       const int col = nt * kBN + n;
-      const int slot2 = (nt == u0 / KT) ? 0 : 1;
-      float* part = p.partial + ((int64_t)(cta * 2 + slot2) * NB) * kBN;
-      for (int cb = g * 16; cb < NB; cb += kTc2Groups * 16) {
-        uint32_t r[16];
-        tmem_ld_32x32b_x16(tmem + lane_off + kTc2AccCol + cb, r);
-        tmem_ld_wait();
+      const bool mine = g == 0 || two;
+      const int slot2 = (np == u0 / KT) ? 0 : 1;
+      float* part = p.partial + (((int64_t)(cta * 2 + slot2) * 2 + g) * NB) * kBN;
+      if (mine) {
+        for (int cb = 0; cb < NB; cb += 16) {
+          uint32_t r[16];
+          tmem_ld_32x32b_x16(tmem + lane_off + kTc2AccCol + g * 128 + cb, r);
+          tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int m = cb + j;
-          if (m < p.M) {
-            const float v = __uint_as_float(r[j]);
-            if (complete) p.Y[(int64_t)m * p.ldy + col] = __float2half_rn(v);
-            else __stcg(part + (int64_t)m * kBN + n, v);
+          for (int j = 0; j < 16; ++j) {
+            const int m = cb + j;
+            if (m < p.M) {
+              const float v = __uint_as_float(r[j]);
+              if (complete) p.Y[(int64_t)m * p.ldy + col] = __float2half_rn(v);
+              else __stcg(part + (int64_t)m * kBN + n, v);
+            }
           }
         }
       }
@@ -343,22 +380,38 @@ __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_consta
         if (threadIdx.x == 64) {
           const int lo = (int)((((int64_t)ua + 1) * grid - 1) / p.units);
           const int hi = (int)((((int64_t)ub) * grid - 1) / p.units);
-          const int prev = atomicAdd(&p.sem[nt], 1);
+          const int prev = atomicAdd(&p.sem[np], 1);
           flag[0] = (prev == hi - lo) ? 1 : 0;
           flag[1] = lo;
           flag[2] = hi;
-          flag[3] = ((int)((int64_t)lo * p.units / grid) / KT == nt) ? 0 : 1;
+          flag[3] = ((int)((int64_t)lo * p.units / grid) / KT == np) ? 0 : 1;
         }
         named_bar_sync(1, kTc2Groups * 128);
-        if (flag[0]) {
+        if (flag[0] && mine) {
           __threadfence();
           const int lo = flag[1], hi = flag[2];
-          for (int m = g; m < p.M; m += kTc2Groups) {
-            const float sum = streamk_sum(p.partial, lo, hi, flag[3], (int64_t)NB * kBN, (int64_t)m * kBN + n);
-            p.Y[(int64_t)m * p.ldy + col] = __float2half_rn(sum);
+          // rows in blocks of 8: the (8 x contributors) partial loads of a block are independent
+          // and in flight together; each element is summed in fixed CTA order (reading R12)
+          const float* pb = p.partial + (int64_t)g * NB * kBN;
+          const int64_t sstride = (int64_t)2 * NB * kBN;
+          for (int m0 = 0; m0 < p.M; m0 += 8) {
+            float acc[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+            for (int qc = lo; qc <= hi; ++qc) {
+              const float* src = pb + (int64_t)(qc * 2 + (qc == lo ? flag[3] : 0)) * sstride + n;
+              float v[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) v[j] = (m0 + j < p.M) ? __ldcg(src + (int64_t)(m0 + j) * kBN) : 0.f;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) acc[j] += v[j];
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (m0 + j < p.M) p.Y[(int64_t)(m0 + j) * p.ldy + col] = __float2half_rn(acc[j]);
           }
-          if (threadIdx.x == 64) p.sem[nt] = 0;
         }
+        if (flag[0] && threadIdx.x == 64) p.sem[np] = 0;
         named_bar_sync(1, kTc2Groups * 128);
       }
       ++seg;
@@ -372,9 +425,15 @@ __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_consta
 
 template <class F>
 tl_status launch_tc2(const Tc2Params& p, const CUtensorMap* tmap, int grid, uint32_t smem_bytes, cudaStream_t st) {
-  if (prepare_kernel(reinterpret_cast<const void*>(tc2_kernel<F>), 227 * 1024, kTc2Threads) == 0)
-    return fail(TL_ECUDA, "tc2_kernel: %s", tl_last_error());
-  tc2_kernel<F><<<grid, kTc2Threads, smem_bytes, st>>>(*tmap, p);
+  if (p.G < kBK) {
+    if (prepare_kernel(reinterpret_cast<const void*>(tc2_kernel<F, true>), 227 * 1024, kTc2Threads) == 0)
+      return fail(TL_ECUDA, "tc2_kernel: %s", tl_last_error());
+    tc2_kernel<F, true><<<grid, kTc2Threads, smem_bytes, st>>>(*tmap, p);
+  } else {
+    if (prepare_kernel(reinterpret_cast<const void*>(tc2_kernel<F, false>), 227 * 1024, kTc2Threads) == 0)
+      return fail(TL_ECUDA, "tc2_kernel: %s", tl_last_error());
+    tc2_kernel<F, false><<<grid, kTc2Threads, smem_bytes, st>>>(*tmap, p);
+  }
   return check_launch("tc2_kernel");
 }
 

@@ -513,38 +513,52 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_tma[s]);
         tcd_istamp(p, dw, lane, kk, 2);
-        if (t >= kTcdNW) mbar_wait(&full_acc[(t - kTcdNW) % NACC], (uint32_t)((t - kTcdNW) / NACC) & 1);
         const uint32_t tslot = tmem + lane_off + wsl * 64;
-        tcd_istamp(p, dw, lane, kk, 3);
-        if (!(TCD_TRACE_ON && (p.dbg & 4))) {
-          // per-P constants -(2^(10-P) + z) (exact: integers below 2048)
-          uint32_t cp[10];
-          static_for<0, 10>([&](auto PP) {
-            constexpr int P = decltype(PP)::value;
-            if constexpr (kInt && plan_uses_p<F>(P)) {
-              constexpr uint32_t k = 0x8000u | ((uint32_t)(25 - P) << 10);  // fp16 -2^(10-P)
-              cp[P] = h2_as_u32(__hadd2(u32_as_h2(zneg), u32_as_h2(k | (k << 16))));
+        // per-P constants -(2^(10-P) + z) (exact: integers below 2048)
+        uint32_t cp[10];
+        static_for<0, 10>([&](auto PP) {
+          constexpr int P = decltype(PP)::value;
+          if constexpr (kInt && plan_uses_p<F>(P)) {
+            constexpr uint32_t k = 0x8000u | ((uint32_t)(25 - P) << 10);  // fp16 -2^(10-P)
+            cp[P] = h2_as_u32(__hadd2(u32_as_h2(zneg), u32_as_h2(k | (k << 16))));
+          }
+        });
+        // chunk c = pairs 16c .. 16c+15 = the TMEM columns of MMAs 2c, 2c+1
+        auto unpack = [&](auto CC, uint32_t (&r)[16]) {
+          constexpr int c = decltype(CC)::value;
+          constexpr int h = c >> 1;  // block
+          uint32_t bw[2 * F::bits];
+#pragma unroll
+          for (int j = 0; j < 2 * F::bits; ++j) bw[j] = words[tile_word(h, j)];
+          static_for<0, 16>([&](auto II) {
+            constexpr int i = (c & 1) * 16 + decltype(II)::value;  // pair within the block
+            if constexpr (kInt) {
+              constexpr int P = kPlan<F::kind, F::bits, F::exp>.pr[i].P;
+              const uint32_t x = extract_pair<F, i>(bw, p.magic);
+              r[decltype(II)::value] =
+                  h2_as_u32(__hfma2(u32_as_h2(x), u32_as_h2(h2_pow2_neg<P>()), u32_as_h2(cp[P])));
+            } else {
+              r[decltype(II)::value] = extract_pair<F, i>(bw, 0u);
             }
           });
-          static_for<0, 4>([&](auto CC) {
-            constexpr int c = decltype(CC)::value;  // pairs 16c .. 16c+15 = TMEM columns of MMAs 2c, 2c+1
-            constexpr int h = c >> 1;                // block
-            uint32_t bw[2 * F::bits];
+        };
+        // the first half of the unpack runs BEFORE the W^T-slot wait (into registers: the asm
+        // register fences keep the compiler from sinking it below the wait), so a group's
+        // long ALU phase never waits for the in-order MMA of tile t - NW
+        uint32_t r0[16], r1[16];
+        unpack(std::integral_constant<int, 0>{}, r0);
+        unpack(std::integral_constant<int, 1>{}, r1);
 #pragma unroll
-            for (int j = 0; j < 2 * F::bits; ++j) bw[j] = words[tile_word(h, j)];
+        for (int i = 0; i < 16; ++i) asm volatile("" : "+r"(r0[i]), "+r"(r1[i]));
+        if (t >= kTcdNW) mbar_wait(&full_acc[(t - kTcdNW) % NACC], (uint32_t)((t - kTcdNW) / NACC) & 1);
+        tcd_istamp(p, dw, lane, kk, 3);
+        if (!(TCD_TRACE_ON && (p.dbg & 4))) {
+          tcd_sttm_x16(tslot, r0);
+          tcd_sttm_x16(tslot + 16, r1);
+          static_for<2, 4>([&](auto CC) {
             uint32_t r[16];
-            static_for<0, 16>([&](auto II) {
-              constexpr int i = (c & 1) * 16 + decltype(II)::value;  // pair within the block
-              if constexpr (kInt) {
-                constexpr int P = kPlan<F::kind, F::bits, F::exp>.pr[i].P;
-                const uint32_t x = extract_pair<F, i>(bw, p.magic);
-                r[decltype(II)::value] =
-                    h2_as_u32(__hfma2(u32_as_h2(x), u32_as_h2(h2_pow2_neg<P>()), u32_as_h2(cp[P])));
-              } else {
-                r[decltype(II)::value] = extract_pair<F, i>(bw, 0u);
-              }
-            });
-            tcd_sttm_x16(tslot + c * 16, r);
+            unpack(CC, r);
+            tcd_sttm_x16(tslot + decltype(CC)::value * 16, r);
           });
         }
         tcd_istamp(p, dw, lane, kk, 4);
