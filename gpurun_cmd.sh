@@ -1,4 +1,3 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -8 > gpurun_out/t22.log
-for a in "u3 qkv 128" "u3 o 128" "u3 gate_up 128" "u3 down 128" "i5 gate_up 128" "f6e3m2 gate_up 128" "u8 gate_up 128" "u8 qkv 128" "u3 gate_up 64" "u3 gate_up 32"; do timeout 120 python tools/prof_one.py $a >> gpurun_out/p22.txt 2>&1; done
-cat gpurun_out/t22.log; grep "us=" gpurun_out/p22.txt; grep -i error gpurun_out/p22.txt | head -3
+for d in 0; do echo "dbg=$d" >> gpurun_out/gs30.txt; TL_TC2_DBG=$d timeout 200 python tools/grid_sweep.py u3 gate_up 128 2 112 148 >> gpurun_out/gs30.txt 2>&1;  TL_TC2_DBG=$d timeout 200 python tools/grid_sweep.py u3 qkv 128 2 80 120 148 >> gpurun_out/gs30.txt 2>&1; TL_TC2_DBG=$d timeout 200 python tools/grid_sweep.py u3 o 128 2 64 128 148 >> gpurun_out/gs30.txt 2>&1; done
+timeout 600 python -m pytest tests -m gpu -q -x -k "batched or tc" 2>&1 | tail -2 >> gpurun_out/gs30.txt; cat gpurun_out/gs30.txt

@@ -47,6 +47,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait_sleepy(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) __nanosleep(128);
 }
+// for warps that wait a long time (µs): exponential back-off up to ~2 µs
+__device__ __forceinline__ void mbar_wait_lazy(uint64_t* bar, uint32_t parity) {
+  uint32_t ns = 64;
+  while (!mbar_try_wait(bar, parity)) {
+    __nanosleep(ns);
+    if (ns < 2048) ns <<= 1;
+  }
+}
 
 // ---- L2 cache policies ---------------------------------------------------------------
 __device__ __forceinline__ uint64_t policy_evict_first() {

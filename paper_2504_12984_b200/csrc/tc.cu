@@ -169,6 +169,7 @@ tl_status tc_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, cons
     p.partial = partial;
     p.sem = sem;
     p.magic = 0x64006400u;
+    p.dbg = env_dbg("TL_TC2_DBG");
     // stage: [activation boxes NB x 256 B (1024-aligned, 128B swizzle) | weight tile 2p | weight tile 2p+1]
     const uint32_t wb = (uint32_t)tile_bytes(w.bits);
     p.w_off_in_stage = (uint32_t)p.NB * 256;

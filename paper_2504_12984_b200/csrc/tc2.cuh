@@ -46,6 +46,7 @@ struct Tc2Params {
   float* partial;  // [grid][2 slots][2 tiles][NB][128]
   int* sem;        // [n-pairs]
   uint32_t magic;  // 0x64006400 (a kernel argument: the LOP3 takes one immediate, see tcd)
+  int dbg;         // TL_TC2_DBG timing experiments (results invalid): 1 skip partial stores, 2 skip reduction
 };
 
 constexpr int kTc2Groups = 2;
@@ -366,7 +367,7 @@ __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_consta
             if (m < p.M) {
               const float v = __uint_as_float(r[j]);
               if (complete) p.Y[(int64_t)m * p.ldy + col] = __float2half_rn(v);
-              else __stcg(part + (int64_t)m * kBN + n, v);
+              else if (!(p.dbg & 1)) __stcg(part + (int64_t)m * kBN + n, v);
             }
           }
         }
@@ -387,28 +388,57 @@ __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_consta
           flag[3] = ((int)((int64_t)lo * p.units / grid) / KT == np) ? 0 : 1;
         }
         named_bar_sync(1, kTc2Groups * 128);
-        if (flag[0] && mine) {
+        if (flag[0] && !(p.dbg & 2)) {
+          // last contributor: Y = the contributors' partials summed in fixed CTA order (reading
+          // R12).  All 256 threads over the flattened partial tile as float4 (16 B loads, 512 B
+          // per warp row), 4 elements x up to 4 contributors of loads in flight per thread before
+          // any store (the reduction is latency-bound otherwise).
           __threadfence();
           const int lo = flag[1], hi = flag[2];
-          // rows in blocks of 8: the (8 x contributors) partial loads of a block are independent
-          // and in flight together; each element is summed in fixed CTA order (reading R12)
-          const float* pb = p.partial + (int64_t)g * NB * kBN;
           const int64_t sstride = (int64_t)2 * NB * kBN;
-          for (int m0 = 0; m0 < p.M; m0 += 8) {
-            float acc[8];
+          const int tid = threadIdx.x - 64;
+          const int nv = p.M * (kBN / 4);  // float4 per tile
+          for (int tj = 0; tj < (two ? 2 : 1); ++tj) {
+            const float* pb = p.partial + (int64_t)tj * NB * kBN;
+            for (int e0 = tid; e0 < nv; e0 += 4 * kTc2Groups * 128) {
+              float4 acc[4];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-            for (int qc = lo; qc <= hi; ++qc) {
-              const float* src = pb + (int64_t)(qc * 2 + (qc == lo ? flag[3] : 0)) * sstride + n;
-              float v[8];
+              for (int j = 0; j < 4; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+              for (int qb = lo; qb <= hi; qb += 4) {
+                float4 v[4][4];
 #pragma unroll
-              for (int j = 0; j < 8; ++j) v[j] = (m0 + j < p.M) ? __ldcg(src + (int64_t)(m0 + j) * kBN) : 0.f;
+                for (int c = 0; c < 4; ++c) {
+                  const int qc = qb + c;
+                  const float4* src =
+                      reinterpret_cast<const float4*>(pb + (int64_t)(qc * 2 + (qc == lo ? flag[3] : 0)) * sstride);
 #pragma unroll
-              for (int j = 0; j < 8; ++j) acc[j] += v[j];
+                  for (int j = 0; j < 4; ++j) {
+                    const int e = e0 + j * kTc2Groups * 128;
+                    v[c][j] = (qc <= hi && e < nv) ? __ldcg(src + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+                  }
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                  for (int j = 0; j < 4; ++j)
+                    if (qb + c <= hi) {
+                      acc[j].x += v[c][j].x;
+                      acc[j].y += v[c][j].y;
+                      acc[j].z += v[c][j].z;
+                      acc[j].w += v[c][j].w;
+                    }
+              }
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int e = e0 + j * kTc2Groups * 128;
+                if (e < nv) {
+                  const int m = e >> 5, c4 = e & 31;  // kBN / 4 == 32 float4 per row
+                  const uint2 o = make_uint2(h2_as_u32(__floats2half2_rn(acc[j].x, acc[j].y)),
+                                             h2_as_u32(__floats2half2_rn(acc[j].z, acc[j].w)));
+                  *reinterpret_cast<uint2*>(p.Y + (int64_t)m * p.ldy + (2 * np + tj) * kBN + 4 * c4) = o;
+                }
+              }
             }
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              if (m0 + j < p.M) p.Y[(int64_t)(m0 + j) * p.ldy + col] = __float2half_rn(acc[j]);
           }
         }
         if (flag[0] && threadIdx.x == 64) p.sem[np] = 0;
