@@ -1,3 +1,12 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-for d in 0; do echo "dbg=$d" >> gpurun_out/gs30.txt; TL_TC2_DBG=$d timeout 200 python tools/grid_sweep.py u3 gate_up 128 2 112 148 >> gpurun_out/gs30.txt 2>&1;  TL_TC2_DBG=$d timeout 200 python tools/grid_sweep.py u3 qkv 128 2 80 120 148 >> gpurun_out/gs30.txt 2>&1; TL_TC2_DBG=$d timeout 200 python tools/grid_sweep.py u3 o 128 2 64 128 148 >> gpurun_out/gs30.txt 2>&1; done
-timeout 600 python -m pytest tests -m gpu -q -x -k "batched or tc" 2>&1 | tail -2 >> gpurun_out/gs30.txt; cat gpurun_out/gs30.txt
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -3 > gpurun_out/t31.log
+timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/b31.json 2> gpurun_out/b31.err
+cat gpurun_out/t31.log; tail -2 gpurun_out/b31.err; python - <<'PY'
+import json
+d=json.loads(open('gpurun_out/b31.json').read().strip().splitlines()[-1])
+print(d['value'], d['ms_per_step'], d['roofline']['frac'], d['e2e']['value'], d['clocks'])
+for x in d['details']: print('M1', x['fmt'], x['layer'], x['us'], x['hbm_frac'])
+for x in d['details_extra_M']: print('M%d'%x['M'], x['fmt'], x['layer'], x['us'], x['TFLOPs'], x['tensor_frac_fp16'])
+for x in d['details_c5'] or []: print('C5', x)
+print(d.get('cpu_baseline'))
+PY

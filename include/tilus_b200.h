@@ -168,8 +168,9 @@ tl_status tl_matmul_hostio(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t
                            const void* zeros, void* Y_dev, void* Y_host, void* workspace,
                            size_t workspace_bytes, uint32_t flags, void* stream);
 
-/* Which family (tl_path) and split-K grid tl_matmul would use for this problem on the current
- * device (for the bench and the dispatch sweep); *splits_out = 0 means one CTA per SM. */
+/* Which family (tl_path) and split-K grid (CTAs; 0 = the CUDA-core path's occupancy-sized grid)
+ * tl_matmul would use for this problem on the current device (for the bench and the dispatch
+ * sweep).  The rule is DESIGN.md "Dispatch". */
 tl_status tl_matmul_plan(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group,
                          int32_t* path_out, int32_t* splits_out);
 

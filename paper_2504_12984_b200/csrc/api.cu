@@ -104,11 +104,18 @@ size_t tl_matmul_workspace_bytes(tl_wtype w, tl_atype a, int64_t M, int64_t N, i
 tl_status tl_matmul_plan(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group,
                          int32_t* path_out, int32_t* splits_out) {
   if (a != TL_ACT_F16) return fail(TL_EUNSUPPORTED, "activation type %d is not supported by this build", (int)a);
-  (void)N;
   (void)K;
-  (void)group;
-  if (path_out) *path_out = choose_path(w, M, group);
-  if (splits_out) *splits_out = 0;
+  int path = choose_path(w, M, group);
+  if (path == TL_PATH_TCD && !tcd_eligible(M, group)) path = TL_PATH_TC;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (sms > 160) sms = 160;
+  int splits = 0;
+  if (path == TL_PATH_TCD) splits = splitk_grid((int)(N / kBN), sms, false);
+  if (path == TL_PATH_TC) splits = splitk_grid((int)((N / kBN + 1) / 2), sms, true);
+  if (path_out) *path_out = path;
+  if (splits_out) *splits_out = splits;
   return TL_OK;
 }
 

@@ -60,7 +60,7 @@ tl_status tcd_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, con
     if (!g_trace) cudaMalloc(&g_trace, 2 * 16 * 256 * sizeof(long long));
     p.trace = g_trace + (launches++ & 1) * 16 * 256;
   }
-  int grid = grid_req > 0 ? grid_req : sms;
+  int grid = grid_req > 0 ? grid_req : splitk_grid((int)(N / kBN), sms, false);
   if (grid > 160) grid = 160;
   if (grid > p.units) grid = p.units;
   // decode (M = 1) with the activation row resident in shared memory (TcdCfg<1>): K*2 <= 64 KB
@@ -107,6 +107,25 @@ size_t tcd_workspace_bytes(int64_t M, int64_t N, int64_t K) {
 constexpr int kTcMaxCtas = 160;
 
 static int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+// Split-K grid (row a2 / a10; measured): `work` = independent output blocks
+// (n-tiles for tcd, n-pairs for tc2), `sms` = SMs.  When a whole multiple S >= 2 of the blocks fits
+// the SMs, every block is split into exactly S CTAs (ranges aligned to block boundaries: each
+// stream-K reduction has S equal contributors that finish together); when there are more
+// blocks than SMs, the grid is the smallest that gives every CTA the same number of WHOLE blocks
+// if that loses little, else one CTA per SM (stream-K).  `expensive_partials`: the batched
+// kernel's fp32 partial tiles are up to 128 KB per CTA, the decode kernel's 0.5-8 KB.
+int splitk_grid(int work, int sms, bool expensive_partials) {
+  if (work <= 0) return 1;
+  if (work <= sms) {
+    const int S = sms / work;
+    if (expensive_partials) return S * work;                  // aligned splits always win (tc2)
+    return (S >= 2 && S * work * 100 >= 85 * sms) ? S * work : sms;  // tcd: only near-full grids
+  }
+  const int per = (work + sms - 1) / sms;  // whole blocks per CTA
+  const int g = (work + per - 1) / per;
+  return (expensive_partials && work % per == 0) ? g : sms;
+}
 
 size_t tc_workspace_bytes(int64_t M, int64_t N, int64_t K) {
   (void)N;
@@ -185,7 +204,7 @@ tl_status tc_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, cons
     CUtensorMap tmap;
     tl_status s = make_tmap_a(&tmap, A + m0 * lda, mc, K, lda, p.NB);
     if (s != TL_OK) return s;
-    int grid = grid_req > 0 ? grid_req : sms;
+    int grid = grid_req > 0 ? grid_req : splitk_grid((p.NT + 1) / 2, sms, true);
     if (grid > kTcMaxCtas) grid = kTcMaxCtas;
     if (grid > p.units) grid = p.units;
     s = TL_EUNSUPPORTED;
