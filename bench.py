@@ -377,6 +377,9 @@ def run_ours(args):
                "d2h_bytes_per_step": sum(2 * M * p["N"] for p in probs),
                "ms_per_step": round(ems / args.steps, 4)}
 
+    # ---- north-star coverage: all 37 formats x 70B layers x M in {1, 16} (rank 0 only) ----
+    spectrum = run_spectrum(args, P, torch, dev, peaks) if (rank == 0 and not args.no_spectrum) else None
+
     # ---- C5 (BASELINE configs[4]): Llama-3.3-70B gate_up strong-scaled over the ranks ----
     c5 = None if args.no_c5 else run_c5(args, P, torch, dist, world, rank, dev, peaks)
 
@@ -399,12 +402,53 @@ def run_ours(args):
             "details": details,
             "details_extra_M": extra,
             "details_c5": c5,
+            "details_spectrum": spectrum,
         }
         if world == 1 and not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline(args.formats, layers, G, M)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_spectrum(args, P, torch, dev, peaks):
+    """North-star coverage (every bit width 1-8, int / uint / float, PAPER.md:518-523 fig:exp_coverage):
+    all 37 kernel formats on the four Llama-3.3-70B layers at M = 1 and M = 16 (gate_up at M = 16
+    is the paper's coverage shape BS=16, K=8192, N=57344).  Device time of one tl_matmul_ex per
+    (format, layer, M), 10 back-to-back launches after 3 warm-ups; algorithmic GB/s and the fraction
+    of the measured HBM copy bandwidth."""
+    from oracle import all_kernel_formats
+    G = 128
+    out = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for f in all_kernel_formats():
+        fmt = f.name
+        w = P.wtype(fmt)
+        for lname, (K, N) in wl.LLAMA33_70B.items():
+            seed = wl.stable_seed("spectrum", fmt, lname)
+            codes = wl.gen_codes_torch(fmt, K, N, seed, dev)
+            wt = P.tl_transform_weights(w, K, N, P.tl_pack(w, K, N, codes))
+            del codes
+            s = wl.gen_scales_torch(fmt, K, N, G, seed, dev)
+            z = wl.gen_zeros_torch(fmt, K, N, G, seed, dev)
+            ws = torch.zeros(P.tl_matmul_workspace_bytes(w, 16, N, K, G), dtype=torch.uint8, device=dev)
+            for M in (1, 16):
+                A = wl.gen_activations_torch(M, K, seed, dev)
+                Y = torch.empty((M, N), dtype=torch.float16, device=dev)
+                for _ in range(3):
+                    P.tl_matmul_ex(w, M, N, K, G, A, wt, s, z, Y, ws, flags=P.TL_FLAG_STATIC_WEIGHTS)
+                e0.record()
+                for _ in range(10):
+                    P.tl_matmul_ex(w, M, N, K, G, A, wt, s, z, Y, ws, flags=P.TL_FLAG_STATIC_WEIGHTS)
+                e1.record()
+                torch.cuda.synchronize()
+                us = e0.elapsed_time(e1) / 10 * 1e3
+                b = alg_bytes(fmt, M, K, N, G)
+                out.append({"fmt": fmt, "layer": lname, "M": M, "us": round(us, 2),
+                            "GBps": round(b / (us * 1e-6) / 1e9, 1),
+                            "hbm_frac": round(b / (us * 1e-6) / 1e9 / peaks["hbm_gbs"], 3)})
+            del wt, s, z, ws
+    return out
 
 
 def run_c5(args, P, torch, dist, world, rank, dev, peaks):
@@ -502,6 +546,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c5", action="store_true", help="skip the strong-scaled gate_up (configs[4]) block")
+    ap.add_argument("--no-spectrum", action="store_true", help="skip the 37-format coverage table")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # `python bench.py --gpus N`: start the N ranks ourselves (one process per GPU, NCCL)

@@ -1,12 +1,4 @@
-# one GPU session (round 2): parity suite, smoke, bench line, ncu launch list of the bench step (time + DRAM
-# bytes per launch), ncu --set full of the decode kernel (u3 gate_up M=1) and the batched kernel (u3 gate_up M=128)
-cd $GRAFT_REPO_ROOT
-mkdir -p gpurun_out
-TAG=${TAG:-r2}
-timeout -s KILL 900 python -m pytest tests -m gpu -q 2>&1 | tail -5 > gpurun_out/${TAG}_pytest_gpu.log
-timeout -s KILL 120 python __graft_entry__.py smoke > gpurun_out/${TAG}_smoke.log 2>&1
-timeout -s KILL 600 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
-timeout -s KILL 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 600 --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 3 --no-extra --no-e2e --no-cpu --no-c5 > /dev/null 2> gpurun_out/${TAG}_ncu_launch.err
-timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:tcd_kernel -s 6 -c 1 -o gpurun_out/${TAG}_tcd_u3_gateup_m1 python tools/prof_one.py u3 gate_up 1 > /dev/null 2>> gpurun_out/${TAG}_ncu_full.err
-timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:tc2_kernel -s 6 -c 1 -o gpurun_out/${TAG}_tc2_u3_gateup_m128 python tools/prof_one.py u3 gate_up 128 > /dev/null 2>> gpurun_out/${TAG}_ncu_full.err
-cat gpurun_out/${TAG}_pytest_gpu.log gpurun_out/${TAG}_smoke.log; tail -c 400 gpurun_out/${TAG}_bench.json; tail -3 gpurun_out/${TAG}_bench.err
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+for i in 1 2 3; do for f in u8 u7 f8e4m3 u3; do for l in down gate_up qkv o; do timeout 60 python tools/grid_sweep.py $f $l 1 1 0 >> gpurun_out/gv40.txt 2>&1 || echo "FAIL $f $l" >> gpurun_out/gv40.txt; done; done; done
+timeout 300 compute-sanitizer --tool memcheck python tools/run_shape.py u8 28672 8192 1 1 > gpurun_out/san40.txt 2>&1; tail -3 gpurun_out/san40.txt
+grep -c "us=" gpurun_out/gv40.txt; grep "FAIL" gpurun_out/gv40.txt | sort | uniq -c

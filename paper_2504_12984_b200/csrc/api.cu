@@ -150,6 +150,13 @@ tl_status tl_matmul_ex(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, 
   int* sem = reinterpret_cast<int*>(workspace);
   float* partial = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(workspace) + kSemBytes);
   cudaStream_t s = as_stream(stream);
+  if (path == TL_PATH_GEMV && gv1_eligible(M, K, group) && env_int("TL_OLD_GEMV", 0) == 0) {
+    tl_status r = gv1_matmul(w, N, K, group, reinterpret_cast<const __half*>(A), reinterpret_cast<const uint8_t*>(w_t),
+                             reinterpret_cast<const __half*>(scales), reinterpret_cast<const __half*>(zeros),
+                             reinterpret_cast<__half*>(Y), partial, sem, splits,
+                             (flags & TL_FLAG_STATIC_WEIGHTS) != 0, s);
+    if (r != TL_ENOFIT) return r;
+  }
   if (path == TL_PATH_GEMV) {
     if (M > 16) {
       // the CUDA-core path handles up to 16 rows per launch

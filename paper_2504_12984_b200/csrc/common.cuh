@@ -242,6 +242,22 @@ __device__ __forceinline__ void load_block_words(const uint8_t* tile, int c, uin
   }
 }
 
+// ---- scale / zero rows of a weight stage (CUDA-core decode kernel gv1) ---------------------
+// The [K/G, N] scale (and zero-point) array is viewed as a 3-D tensor {128 columns, K/G rows,
+// N/128 n-tiles} (strides N*2 and 256 bytes); one box of {128, R, 1} brings the rows of up to R
+// consecutive k-tiles of ONE n-tile.  A stage of R consecutive units spans at most two n-tiles
+// (segment 0: the first tile's n-tile, segment 1: the next), so its side area holds two regions
+// of R rows per array: [scales seg0 | scales seg1 | zeros seg0 | zeros seg1], 256 B per row.
+__host__ __device__ constexpr uint32_t side_bytes(int R) { return (uint32_t)R * 4u * 256u; }
+
+// byte offset, within the side area, of the scale row of a tile at k-tile kt of n-tile nt in a
+// stage whose first unit is (nt0, kt0); add R*512 for its zero row
+__device__ __forceinline__ uint32_t side_row_off(int R, int tpg, int nt, int kt, int nt0, int kt0) {
+  const int seg = nt != nt0;
+  const int first = seg ? 0 : kt0;
+  return (uint32_t)(seg * R + kt / tpg - first / tpg) * 256u;
+}
+
 // Deterministic stream-K reduction (reading R12) of one output element of n-tile nt: the partial
 // tiles of CTAs lo..hi summed in CTA order.  CTA q keeps two partial slots (0: its first n-tile,
 // 1: its last); every q > lo starts inside nt (slot 0), only q == lo may have started earlier

@@ -22,6 +22,10 @@ struct GemvParams {
 };
 
 tl_status gemv_dispatch(tl_wtype w, const GemvParams& p, int grid_req, cudaStream_t st);
+bool gv1_eligible(int64_t M, int64_t K, int32_t G);
+tl_status gv1_matmul(tl_wtype w, int64_t N, int64_t K, int32_t G, const __half* A, const uint8_t* wt,
+                     const __half* scales, const __half* zeros, __half* Y, float* partial, int* sem, int grid_req,
+                     bool static_weights, cudaStream_t st);
 size_t gemv_workspace_bytes(int64_t M, int64_t N, int64_t K);
 
 // CTAs the GEMV workspace holds partial slots for (the grid is clamped to it)

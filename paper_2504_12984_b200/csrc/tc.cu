@@ -163,6 +163,23 @@ static tl_status make_tmap_a(CUtensorMap* m, const __half* A, int64_t M, int64_t
   return TL_OK;
 }
 
+// The [K/G, N] scale / zero array as a 3-D tensor {128 columns, K/G rows, N/128 n-tiles}
+// (strides N*2 and 256 bytes): boxes {128, R, 1} = the rows of R consecutive k-tiles of one n-tile
+// (common.cuh side_row_off).  Rows past K/G are zero-filled.
+tl_status make_tmap_side(CUtensorMap* m, const __half* X, int64_t N, int64_t K, int32_t G, int R) {
+  auto enc = get_encode();
+  if (!enc) return fail(TL_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)kBN, (cuuint64_t)(K / G), (cuuint64_t)(N / kBN)};
+  cuuint64_t strides[2] = {(cuuint64_t)(N * 2), (cuuint64_t)(kBN * 2)};
+  cuuint32_t box[3] = {(cuuint32_t)kBN, (cuuint32_t)R, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<__half*>(X), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TL_ECUDA, "cuTensorMapEncodeTiled (scales) failed (%d)", (int)r);
+  return TL_OK;
+}
+
 tl_status tc_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, const __half* A, int64_t lda,
                     const uint8_t* wt, const __half* scales, const __half* zeros, __half* Y, int64_t ldy,
                     float* partial, int* sem, int grid_req, cudaStream_t st) {

@@ -16,7 +16,7 @@ __device__ __forceinline__ uint64_t sw128(uint32_t saddr) {
   return d;
 }
 
-__global__ void mma_kernel(int N, int ts, int reps, long long* out) {
+__global__ void mma_kernel(int N, int ts, int reps, int nd, long long* out) {
   extern __shared__ __align__(1024) uint8_t sm[];  // A: 128 rows x 128 B (16 KB), B: 256 rows x 128 B (32 KB)
   __shared__ uint64_t bar;
   __shared__ uint32_t slot;
@@ -52,12 +52,12 @@ __global__ void mma_kernel(int N, int ts, int reps, long long* out) {
           if (ts) {
             asm volatile(
                 "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
+                "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem + (j % nd) * N),
                 "r"(tmem + 256 + j * 8), "l"(bd[j & 3]), "r"(idesc), "r"(1u));
           } else {
             asm volatile(
                 "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + (j % nd) * N),
                 "l"(ad[j & 3]), "l"(bd[j & 3]), "r"(idesc), "r"(1u));
           }
         }
@@ -82,17 +82,19 @@ int main() {
   long long* d;
   cudaMalloc(&d, 16);
   cudaFuncSetAttribute(mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 49152 + 1024);
-  for (int ts = 0; ts < 2; ++ts)
-    for (int N : {16, 32, 64, 128, 256}) {
-      const int reps = 4096;
-      for (int grid : {1, 148}) {
-        mma_kernel<<<grid, 128, 49152 + 1024>>>(N, ts, reps, d);
+  for (int ts = 1; ts >= 0; --ts)
+    for (int N : {16, 32, 64, 128})
+      for (int nd : {1, 2, 4, 8}) {
+        if (nd * N > 256) continue;
+        const int reps = 4096;
+        const int grid = 148;
+        mma_kernel<<<grid, 128, 49152 + 1024>>>(N, ts, reps, nd, d);
         cudaError_t e = cudaDeviceSynchronize();
         long long h[2];
         cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
-        printf("%s N=%3d grid=%3d: issue %.1f cyc/mma, complete %.1f cyc/mma  (%s)\n", ts ? "TS" : "SS", N, grid,
-               (double)h[0] / reps, (double)h[1] / reps, e == cudaSuccess ? "ok" : cudaGetErrorString(e));
+        printf("%s N=%3d independent accumulators=%d: issue %.1f cyc/mma, complete %.1f cyc/mma  (%s)\n",
+               ts ? "TS" : "SS", N, nd, (double)h[0] / reps, (double)h[1] / reps,
+               e == cudaSuccess ? "ok" : cudaGetErrorString(e));
       }
-    }
   return 0;
 }
