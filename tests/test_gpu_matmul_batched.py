@@ -190,3 +190,30 @@ def test_full_size_sampled_columns_batched(env, fmt, layer, M):
     w = dequant(parse_wtype(fmt), codes[:, cols], s[:, cols], zc, G)
     r = tolerance_check(Y[:, cols], Y64, A, w)
     assert r["ok"] and r["max_abs_ratio"] <= 1e-3, r
+
+
+@pytest.mark.parametrize("path", [GEMV, TCD, 0], ids=["gemv", "tcd", "auto"])
+@pytest.mark.parametrize("K,G", [(40960, 128), (2048, 256), (2048, 2048), (1536, 384)])
+@pytest.mark.parametrize("fmt", ["u3", "i6", "f6e3m2", "u8"])
+def test_decode_configurations(env, fmt, K, G, path):
+    """M = 1 beyond the common shape: K*2 > 64 KB (the activation row no longer fits the decode
+    kernels' shared-memory stash: tcd runs its 16-row configuration, the CUDA-core GEMV falls back
+    to the staged kernel) and groups spanning several 128-k tiles (G = 256, 384, K)."""
+    P, torch = env
+    N = 256
+    A, codes, s, z = make_problem(fmt, 1, K, N, G, seed_tag="decode-cfg")
+    Y, _, _ = run_matmul(P, torch, fmt, A, codes, s, z, G, path=path)
+    check_oracle(fmt, A, codes, s, z, G, Y)
+
+
+@pytest.mark.parametrize("splits", [1, 2, 5, 40, 148])
+@pytest.mark.parametrize("fmt", ["u3", "f6e3m2"])
+def test_gemv_m1_stream_k(env, fmt, splits):
+    """The M = 1 CUDA-core kernel under every stream-K partition: n-tile segments shared by several
+    CTAs, stages that span two n-tiles (their scale / zero boxes come from two n-tiles)."""
+    P, torch = env
+    K, N, G = 1536, 640, 128
+    A, codes, s, z = make_problem(fmt, 1, K, N, G, seed_tag="gv1-sk")
+    Y, full, _ = run_matmul(P, torch, fmt, A, codes, s, z, G, path=GEMV, splits=splits, ldy=N + 8)
+    assert np.isnan(full[:, N:]).all()
+    check_oracle(fmt, A, codes, s, z, G, Y)

@@ -21,4 +21,3 @@ u4 1024 512 1 1 5
 i3 1024 512 3 1 5
 LIST
 cat $OUT
-timeout 900 python -m pytest tests -m gpu -q -x -k "decode_configurations or gemv_m1_stream_k" 2>&1 | tail -3
