@@ -1,24 +1,4 @@
-# compute-sanitizer memcheck / racecheck / synccheck over small shapes of every kernel family
-# (explicit synchronisation between in-flight operations that share memory).
-cd $GRAFT_REPO_ROOT
-mkdir -p gpurun_out
-OUT=gpurun_out/${TAG:-r2}_sanitizer.txt
-: > $OUT
-# fmt K N M path splits
-while read fmt K N M path splits; do
-  for tool in memcheck racecheck synccheck; do
-    echo "== $tool $fmt K=$K N=$N M=$M path=$path splits=$splits" >> $OUT
-    timeout -s KILL 300 compute-sanitizer --tool $tool --print-limit 5 python tools/run_shape.py $fmt $K $N $M $path $splits 2>&1 \
-      | grep -E "ERROR SUMMARY|RACECHECK SUMMARY|Error|error|hazard| ok " | head -8 >> $OUT
-  done
-done <<'LIST'
-u4 1024 512 1 3 5
-u4 1024 512 4 3 5
-f6e3m2 1024 512 1 3 3
-u3 1024 512 64 2 5
-i5 1024 768 128 2 7
-u4 1024 512 1 1 5
-i3 1024 512 3 1 5
-LIST
-cat $OUT
-timeout 900 python -m pytest tests -m gpu -q -x -k "decode_configurations or gemv_m1_stream_k" 2>&1 | tail -3
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q -x -k "prefill" 2>&1 | tail -4
+for M in 256 512 1024 2048 4096 8192; do for pth in 2 4; do timeout 120 python tools/grid_sweep.py u4 gate_up $M $pth 0 2>&1 | grep "us="; done; done
+for M in 512 1024 4096; do for pth in 2 4; do timeout 120 python tools/grid_sweep.py u4 qkv $M $pth 0 2>&1 | grep "us="; done; done

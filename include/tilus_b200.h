@@ -81,8 +81,11 @@ typedef enum {
  *                 tensor memory as exact fp16 values, scale / zero point applied per tile in fp32,
  *                 launched with programmatic dependent launch (see TL_FLAG_STATIC_WEIGHTS).  Falls
  *                 back to TL_PATH_TC outside that range.
+ *   TL_PATH_PREFILL  large M: the weight decoded to fp16 in L2-sized column chunks
+ *                 of the workspace by this library's kernel, then a cuBLAS f16 x f16 GEMM with fp32
+ *                 accumulation per chunk.  The workspace then holds up to 32 MB + 64 MB.
  * TL_PATH_AUTO: the measured dispatch rule. */
-typedef enum { TL_PATH_AUTO = 0, TL_PATH_GEMV = 1, TL_PATH_TC = 2, TL_PATH_TCD = 3 } tl_path;
+typedef enum { TL_PATH_AUTO = 0, TL_PATH_GEMV = 1, TL_PATH_TC = 2, TL_PATH_TCD = 3, TL_PATH_PREFILL = 4 } tl_path;
 
 /* tl_matmul_ex / tl_matmul_hostio flags.
  *   TL_FLAG_STATIC_WEIGHTS  w_t, scales and zeros are not written by any kernel that may still be

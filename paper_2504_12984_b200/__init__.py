@@ -10,13 +10,13 @@ The library must be built (``python paper_2504_12984_b200/build.py``); there is
 no CPU fallback.
 """
 
-from ._lib import (TL_PATH_AUTO, TL_PATH_GEMV, TL_PATH_TC, TL_PATH_TCD, TL_ACT_F16, TL_ACT_BF16, TL_FLAG_STATIC_WEIGHTS, EXPORTED, LIB_PATH, TilusError, alloc_workspace,
+from ._lib import (TL_PATH_AUTO, TL_PATH_GEMV, TL_PATH_TC, TL_PATH_TCD, TL_PATH_PREFILL, TL_ACT_F16, TL_ACT_BF16, TL_FLAG_STATIC_WEIGHTS, EXPORTED, LIB_PATH, TilusError, alloc_workspace,
                    tl_dequant, tl_format_version, tl_matmul, tl_matmul_ex, tl_matmul_hostio, tl_matmul_plan,
                    tl_matmul_workspace_bytes, tl_pack, tl_packed_bytes, tl_transform_weights,
                    tl_transformed_bytes, tl_unpack, tl_untransform_weights, tl_wtype, wtype)
 
 __all__ = [
-    "TL_PATH_AUTO", "TL_PATH_GEMV", "TL_PATH_TC", "TL_PATH_TCD", "TL_ACT_F16", "TL_ACT_BF16", "TL_FLAG_STATIC_WEIGHTS", "EXPORTED", "LIB_PATH", "TilusError", "alloc_workspace",
+    "TL_PATH_AUTO", "TL_PATH_GEMV", "TL_PATH_TC", "TL_PATH_TCD", "TL_PATH_PREFILL", "TL_ACT_F16", "TL_ACT_BF16", "TL_FLAG_STATIC_WEIGHTS", "EXPORTED", "LIB_PATH", "TilusError", "alloc_workspace",
     "tl_dequant", "tl_format_version", "tl_matmul", "tl_matmul_ex", "tl_matmul_hostio", "tl_matmul_plan",
     "tl_matmul_workspace_bytes", "tl_pack", "tl_packed_bytes", "tl_transform_weights", "tl_transformed_bytes",
     "tl_unpack", "tl_untransform_weights", "tl_wtype", "wtype",

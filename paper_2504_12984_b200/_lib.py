@@ -53,7 +53,7 @@ def wtype(name: str) -> tl_wtype:
     return tl_wtype(2, int(m.group(3)), int(m.group(4)), int(m.group(5)))
 
 
-TL_PATH_AUTO, TL_PATH_GEMV, TL_PATH_TC, TL_PATH_TCD = 0, 1, 2, 3
+TL_PATH_AUTO, TL_PATH_GEMV, TL_PATH_TC, TL_PATH_TCD, TL_PATH_PREFILL = 0, 1, 2, 3, 4
 TL_ACT_F16, TL_ACT_BF16 = 0, 1
 TL_FLAG_STATIC_WEIGHTS = 1
 

@@ -42,6 +42,11 @@ int prepare_kernel(const void* fn, int smem_bytes, int threads) {
   return n;
 }
 
+// M from which decode-to-fp16 + cuBLAS GEMM beats the fused batched kernel (measured, DESIGN.md
+// "Dispatch")
+constexpr int64_t kPrefillM = 512;
+static bool prefill_wins(int64_t M, int64_t N);
+
 // Workspace: [semaphores: 64 KiB][partials ...]
 constexpr size_t kSemBytes = 64 * 1024;
 
@@ -53,14 +58,23 @@ static int env_int(const char* name, int dflt) {
 // Path choice (row a2).  PAPER.md:546 used CUDA cores for 1-15 tokens and tensor
 // cores from 16 on an L40S; on B200 the crossover is lower and is set
 // from the measured sweep.
-static int choose_path(tl_wtype w, int64_t M, int32_t G) {
+static bool prefill_wins(int64_t M, int64_t N) {
+  // measured (profiles/r2_prefill.txt): on a wide layer (gate_up, N = 57344) the fused batched
+  // kernel keeps ~1015 TFLOP/s up to M ~ 1.5k, decode + cuBLAS wins from 2048; on narrower layers
+  // (N <= 16384: qkv, o, down) the batched kernel fills the machine worse and decode + GEMM wins
+  // from M = 512
+  return M >= 2048 || (M >= kPrefillM && N <= 16384);
+}
+
+static int choose_path(tl_wtype w, int64_t M, int64_t N, int32_t G) {
   const int forced = env_int("TL_FORCE_PATH", 0);
-  if (forced == TL_PATH_GEMV || forced == TL_PATH_TC || forced == TL_PATH_TCD) return forced;
+  if (forced >= TL_PATH_GEMV && forced <= TL_PATH_PREFILL) return forced;
   (void)w;
   // measured on B200: the tensor-core decode kernel (tcd) for M <= 16 with a group
   // that is a multiple of 128 (it beats the CUDA-core GEMV from M = 1), the CUDA-core GEMV for the
   // remaining decode shapes (G = 32, 64), the tcgen05 GEMM above M = 16
   if (tcd_eligible(M, G)) return TL_PATH_TCD;
+  if (prefill_wins(M, N)) return TL_PATH_PREFILL;
   if (M <= 1) return TL_PATH_GEMV;
   return TL_PATH_TC;
 }
@@ -98,6 +112,10 @@ size_t tl_matmul_workspace_bytes(tl_wtype w, tl_atype a, int64_t M, int64_t N, i
   size_t t = tc_workspace_bytes(M, N, K);
   size_t ts = tcd_workspace_bytes(M, N, K);
   if (ts > t) t = ts;
+  if (prefill_wins(M, N) || env_int("TL_FORCE_PATH", 0) == TL_PATH_PREFILL) {
+    const size_t pf = prefill_workspace_bytes(M, N, K);
+    if (pf > t) t = pf;
+  }
   return kSemBytes + (g > t ? g : t);
 }
 
@@ -105,7 +123,7 @@ tl_status tl_matmul_plan(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K
                          int32_t* path_out, int32_t* splits_out) {
   if (a != TL_ACT_F16) return fail(TL_EUNSUPPORTED, "activation type %d is not supported by this build", (int)a);
   (void)K;
-  int path = choose_path(w, M, group);
+  int path = choose_path(w, M, N, group);
   if (path == TL_PATH_TCD && !tcd_eligible(M, group)) path = TL_PATH_TC;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -128,7 +146,7 @@ tl_status tl_matmul_ex(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, 
   if (a != TL_ACT_F16)
     return fail(TL_EUNSUPPORTED, "activation type %d is not supported by this build (TL_ACT_F16 only)", (int)a);
   if (flags & ~TL_FLAG_STATIC_WEIGHTS) return fail(TL_EINVAL_SHAPE, "unknown flags 0x%x", flags);
-  if (path < TL_PATH_AUTO || path > TL_PATH_TCD) return fail(TL_EUNSUPPORTED, "unknown path %d", path);
+  if (path < TL_PATH_AUTO || path > TL_PATH_PREFILL) return fail(TL_EUNSUPPORTED, "unknown path %d", path);
   if (splits < 0) return fail(TL_EINVAL_SHAPE, "splits=%d < 0", splits);
   if ((st = check_kn(K, N)) != TL_OK) return st;
   if ((st = check_group(K, group)) != TL_OK) return st;
@@ -145,11 +163,20 @@ tl_status tl_matmul_ex(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, 
   if (!workspace || workspace_bytes < need)
     return fail(TL_EWORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
   if (!aligned16(workspace)) return fail(TL_EALIGN, "workspace must be 16-byte aligned");
-  if (path == TL_PATH_AUTO) path = choose_path(w, M, group);
+  if (path == TL_PATH_AUTO) path = choose_path(w, M, N, group);
   if (path == TL_PATH_TCD && !tcd_eligible(M, group)) path = TL_PATH_TC;
   int* sem = reinterpret_cast<int*>(workspace);
   float* partial = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(workspace) + kSemBytes);
   cudaStream_t s = as_stream(stream);
+  if (path == TL_PATH_PREFILL) {
+    if (workspace_bytes < kSemBytes + prefill_workspace_bytes(M, N, K))
+      return fail(TL_EWORKSPACE, "the prefill path needs %zu workspace bytes",
+                  kSemBytes + prefill_workspace_bytes(M, N, K));
+    return prefill_matmul(w, M, N, K, group, reinterpret_cast<const __half*>(A), lda,
+                          reinterpret_cast<const uint8_t*>(w_t), reinterpret_cast<const __half*>(scales),
+                          reinterpret_cast<const __half*>(zeros), reinterpret_cast<__half*>(Y), ldy,
+                          reinterpret_cast<uint8_t*>(workspace) + kSemBytes, s);
+  }
   if (path == TL_PATH_GEMV && gv1_eligible(M, K, group) && env_int("TL_OLD_GEMV", 0) == 0) {
     tl_status r = gv1_matmul(w, N, K, group, reinterpret_cast<const __half*>(A), reinterpret_cast<const uint8_t*>(w_t),
                              reinterpret_cast<const __half*>(scales), reinterpret_cast<const __half*>(zeros),

@@ -175,6 +175,14 @@ __host__ __device__ constexpr BlockPlan make_plan(int kind, int b, int E) {
 template <int KIND, int B, int E>
 inline constexpr BlockPlan kPlan = make_plan(KIND, B, E);
 
+// is P the field position of some pair of the format's plan (ints)?
+template <class F>
+__host__ __device__ constexpr bool plan_has_p(int P) {
+  for (int i = 0; i < 32; ++i)
+    if (kPlan<F::kind, F::bits, F::exp>.pr[i].P == P) return true;
+  return false;
+}
+
 // tile word (0..4b-1, vector-major: word 4v + r is lane r of 16-byte vector v) of block-local
 // word j of block h
 __host__ __device__ constexpr int tile_word(int h, int j) { return (j >> 1) * 4 + 2 * h + (j & 1); }

@@ -217,3 +217,36 @@ def test_gemv_m1_stream_k(env, fmt, splits):
     Y, full, _ = run_matmul(P, torch, fmt, A, codes, s, z, G, path=GEMV, splits=splits, ldy=N + 8)
     assert np.isnan(full[:, N:]).all()
     check_oracle(fmt, A, codes, s, z, G, Y)
+
+
+PREFILL = 4
+
+
+@pytest.mark.parametrize("M", [200, 512, 700])
+@pytest.mark.parametrize("fmt", ["u1", "u4", "i3", "i8", "f4e2m1", "f6e3m2", "u8"])
+def test_prefill_parity(env, fmt, M):
+    """Large-M path: the weight decoded to fp16 by the library, then a dense
+    f16 x f16 GEMM with fp32 accumulation; ragged M, ldy > N, a group size below 128 for one
+    format."""
+    P, torch = env
+    K, N = 1024, 384
+    G = 64 if fmt == "i3" else 128
+    A, codes, s, z = make_problem(fmt, M, K, N, G, seed_tag="prefill")
+    Y, full, _ = run_matmul(P, torch, fmt, A, codes, s, z, G, path=PREFILL, ldy=N + 8)
+    assert np.isnan(full[:, N:]).all()
+    check_oracle(fmt, A, codes, s, z, G, Y)
+
+
+def test_prefill_chunks_and_auto_dispatch(env):
+    """N larger than one decode chunk (several dq16 + GEMM rounds) through the automatic dispatch
+    at M = 640 (>= the prefill threshold)."""
+    P, torch = env
+    fmt, M, K, N, G = "u4", 640, 8192, 4608, 128
+    A, codes, s, z = make_problem(fmt, M, K, N, G, seed_tag="prefill-chunks")
+    Y, _, _ = run_matmul(P, torch, fmt, A, codes, s, z, G)
+    assert P.tl_matmul_plan(P.wtype(fmt), M, N, K, G)[0] == PREFILL
+    cols = wl.sample_columns(N)
+    Y64 = matmul_cols_fp64(parse_wtype(fmt), A, codes[:, cols], s[:, cols], z[:, cols], G)
+    w = dequant(parse_wtype(fmt), codes[:, cols], s[:, cols], z[:, cols], G)
+    r = tolerance_check(Y[:, cols], Y64, A, w)
+    assert r["ok"] and r["max_abs_ratio"] <= 1e-3, r
