@@ -55,9 +55,11 @@ typedef struct {
   uint8_t man_bits;
 } tl_wtype;
 
-/* Activation type: the dtype of A, of the scales and of Y ("A ... float16";
- * PAPER.md:527 "we also support bfloat16").  TL_ACT_BF16 is reserved in this build: calls that
- * pass it return TL_EUNSUPPORTED. */
+/* Activation type: the dtype of A, of the scales, of the zero points and of Y (PAPER.md:170
+ * "A ... float16"; "we also support bfloat16").  bf16 runs on the
+ * tensor-core families (decode, batched, prefill); a TL_PATH_GEMV request with bf16 runs on the
+ * decode / batched tensor-core kernel instead.  The dequantized weight is exact in fp16 and is
+ * rounded once to bf16 where the MMA / GEMM operand is bf16 (reading R9). */
 typedef enum { TL_ACT_F16 = 0, TL_ACT_BF16 = 1 } tl_atype;
 
 typedef enum {
@@ -142,7 +144,7 @@ tl_status tl_untransform_weights(tl_wtype w, int64_t K, int64_t N, const void* w
  * (PAPER.md:439-440), here owned by the caller so calls stay graph-capturable.
  * The workspace must be ZERO-FILLED once when allocated; the kernels leave every semaphore at zero
  * again when they finish, so it can be reused by any later call on the same stream without
- * clearing.  Returns 0 for an unsupported activation type. */
+ * clearing.  Returns 0 for an unknown activation type. */
 size_t tl_matmul_workspace_bytes(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group);
 
 /* Y[M,N] (row stride ldy elements) = A[M,K] (row stride lda elements) x dequant(w_t): the paper's

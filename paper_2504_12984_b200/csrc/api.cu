@@ -106,7 +106,7 @@ const char* tl_last_error(void) { return g_err; }
 size_t tl_matmul_workspace_bytes(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group) {
   (void)w;
   (void)group;
-  if (a != TL_ACT_F16) return 0;
+  if (a != TL_ACT_F16 && a != TL_ACT_BF16) return 0;
   if (M <= 0 || N <= 0 || K <= 0) return kSemBytes;
   size_t g = gemv_workspace_bytes(M, N, K);
   size_t t = tc_workspace_bytes(M, N, K);
@@ -121,9 +121,10 @@ size_t tl_matmul_workspace_bytes(tl_wtype w, tl_atype a, int64_t M, int64_t N, i
 
 tl_status tl_matmul_plan(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group,
                          int32_t* path_out, int32_t* splits_out) {
-  if (a != TL_ACT_F16) return fail(TL_EUNSUPPORTED, "activation type %d is not supported by this build", (int)a);
+  if (a != TL_ACT_F16 && a != TL_ACT_BF16) return fail(TL_EUNSUPPORTED, "unknown activation type %d", (int)a);
   (void)K;
   int path = choose_path(w, M, N, group);
+  if (a == TL_ACT_BF16 && path == TL_PATH_GEMV) path = tcd_eligible(M, group) ? TL_PATH_TCD : TL_PATH_TC;
   if (path == TL_PATH_TCD && !tcd_eligible(M, group)) path = TL_PATH_TC;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -143,8 +144,8 @@ tl_status tl_matmul_ex(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, 
                        void* stream) {
   tl_status st;
   if ((st = check_wtype(w)) != TL_OK) return st;
-  if (a != TL_ACT_F16)
-    return fail(TL_EUNSUPPORTED, "activation type %d is not supported by this build (TL_ACT_F16 only)", (int)a);
+  if (a != TL_ACT_F16 && a != TL_ACT_BF16) return fail(TL_EUNSUPPORTED, "unknown activation type %d", (int)a);
+  const bool bf = a == TL_ACT_BF16;
   if (flags & ~TL_FLAG_STATIC_WEIGHTS) return fail(TL_EINVAL_SHAPE, "unknown flags 0x%x", flags);
   if (path < TL_PATH_AUTO || path > TL_PATH_PREFILL) return fail(TL_EUNSUPPORTED, "unknown path %d", path);
   if (splits < 0) return fail(TL_EINVAL_SHAPE, "splits=%d < 0", splits);
@@ -164,6 +165,8 @@ tl_status tl_matmul_ex(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, 
     return fail(TL_EWORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
   if (!aligned16(workspace)) return fail(TL_EALIGN, "workspace must be 16-byte aligned");
   if (path == TL_PATH_AUTO) path = choose_path(w, M, N, group);
+  // the CUDA-core kernels are fp16-only: bf16 requests run on the tensor-core families
+  if (bf && path == TL_PATH_GEMV) path = tcd_eligible(M, group) ? TL_PATH_TCD : TL_PATH_TC;
   if (path == TL_PATH_TCD && !tcd_eligible(M, group)) path = TL_PATH_TC;
   int* sem = reinterpret_cast<int*>(workspace);
   float* partial = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(workspace) + kSemBytes);
@@ -175,7 +178,7 @@ tl_status tl_matmul_ex(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, 
     return prefill_matmul(w, M, N, K, group, reinterpret_cast<const __half*>(A), lda,
                           reinterpret_cast<const uint8_t*>(w_t), reinterpret_cast<const __half*>(scales),
                           reinterpret_cast<const __half*>(zeros), reinterpret_cast<__half*>(Y), ldy,
-                          reinterpret_cast<uint8_t*>(workspace) + kSemBytes, s);
+                          reinterpret_cast<uint8_t*>(workspace) + kSemBytes, bf, s);
   }
   if (path == TL_PATH_GEMV && gv1_eligible(M, K, group) && env_int("TL_OLD_GEMV", 0) == 0) {
     tl_status r = gv1_matmul(w, N, K, group, reinterpret_cast<const __half*>(A), reinterpret_cast<const uint8_t*>(w_t),
@@ -218,7 +221,7 @@ tl_status tl_matmul_ex(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, 
     tl_status r = tcd_matmul(w, M, N, K, group, reinterpret_cast<const __half*>(A), lda,
                              reinterpret_cast<const uint8_t*>(w_t), reinterpret_cast<const __half*>(scales),
                              reinterpret_cast<const __half*>(zeros), reinterpret_cast<__half*>(Y), ldy, partial, sem,
-                             splits, (flags & TL_FLAG_STATIC_WEIGHTS) != 0, s);
+                             splits, (flags & TL_FLAG_STATIC_WEIGHTS) != 0, bf, s);
     if (r != TL_ENOFIT) return r;
     // the decode kernel's stage ring does not fit shared memory for this shape: batched path
     path = TL_PATH_TC;
@@ -227,7 +230,7 @@ tl_status tl_matmul_ex(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, 
     return tc_matmul(w, M, N, K, group, reinterpret_cast<const __half*>(A), lda,
                      reinterpret_cast<const uint8_t*>(w_t), reinterpret_cast<const __half*>(scales),
                      reinterpret_cast<const __half*>(zeros), reinterpret_cast<__half*>(Y), ldy, partial, sem,
-                     splits, s);
+                     splits, bf, s);
   }
   return fail(TL_EUNSUPPORTED, "unknown path %d", path);
 }
@@ -244,8 +247,7 @@ tl_status tl_matmul_hostio(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t
                            void* Y_dev, void* Y_host, void* workspace, size_t workspace_bytes, uint32_t flags,
                            void* stream) {
   if (M == 0) return TL_OK;
-  if (a != TL_ACT_F16)
-    return fail(TL_EUNSUPPORTED, "activation type %d is not supported by this build (TL_ACT_F16 only)", (int)a);
+  if (a != TL_ACT_F16 && a != TL_ACT_BF16) return fail(TL_EUNSUPPORTED, "unknown activation type %d", (int)a);
   if (!A_host || !A_dev || !Y_dev || !Y_host) return fail(TL_ENULL, "tl_matmul_hostio: NULL pointer");
   cudaStream_t s = as_stream(stream);
   if (cudaMemcpyAsync(A_dev, A_host, (size_t)(M * K * 2), cudaMemcpyHostToDevice, s) != cudaSuccess)

@@ -35,6 +35,7 @@
 // Size = K*N*b/8 bytes exactly (no padding, as PAPER.md:187).
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -196,6 +197,38 @@ struct Fmt {
   static constexpr int man = KIND == kFloat ? BITS - 1 - EXP : 0;
   static constexpr int bias = KIND == kFloat ? (1 << (EXP - 1)) - 1 : 0;
   // words of one 128-k column run, per segment: 4*w
+};
+
+// ---- activation type (tl_atype): A, scales, zero points and Y share it -----------------------
+// fp16 (TL_ACT_F16) or bf16 (TL_ACT_BF16).  The dequantized weight is
+// built exactly in fp16 (u - z, value(code)) and converted where the MMA or the GEMM needs bf16.
+template <bool BF>
+struct Act {
+  // instruction-descriptor a_format / b_format bits of tcgen05.mma.kind::f16 (0 = F16, 1 = BF16)
+  static constexpr uint32_t idesc_ab = BF ? ((1u << 7) | (1u << 10)) : 0u;
+  __device__ static __forceinline__ float to_float(uint32_t bits16) {
+    if constexpr (BF) return __uint_as_float(bits16 << 16);
+    else return __half2float(__ushort_as_half((unsigned short)bits16));
+  }
+  __device__ static __forceinline__ unsigned short from_float(float v) {
+    if constexpr (BF) return __bfloat16_as_ushort(__float2bfloat16_rn(v));
+    else return __half_as_ushort(__float2half_rn(v));
+  }
+  // an exact fp16x2 pair -> the same two values in this type (exact: |value| <= 2^16, <= 8 bits)
+  __device__ static __forceinline__ uint32_t from_h2(uint32_t h) {
+    if constexpr (BF) {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&h));
+      const __nv_bfloat162 b = __floats2bfloat162_rn(f.x, f.y);
+      return *reinterpret_cast<const uint32_t*>(&b);
+    } else {
+      return h;
+    }
+  }
+  // fp16 bits of -z for a zero point given in this type (integer-valued, |z| <= 255: exact)
+  __device__ static __forceinline__ uint32_t neg_zero_h(uint32_t bits16) {
+    if constexpr (BF) return (uint32_t)__half_as_ushort(__float2half_rn(-to_float(bits16)));
+    else return bits16 ^ 0x8000u;
+  }
 };
 
 // ---- PTX helpers ------------------------------------------------------------------

@@ -35,16 +35,16 @@ constexpr tl_status TL_ENOFIT = (tl_status)100;
 size_t tc_workspace_bytes(int64_t M, int64_t N, int64_t K);
 tl_status tc_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, const __half* A, int64_t lda,
                     const uint8_t* wt, const __half* scales, const __half* zeros, __half* Y, int64_t ldy,
-                    float* partial, int* sem, int grid_req, cudaStream_t st);
+                    float* partial, int* sem, int grid_req, bool bf, cudaStream_t st);
 size_t prefill_workspace_bytes(int64_t M, int64_t N, int64_t K);
 tl_status prefill_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, const __half* A, int64_t lda,
                          const uint8_t* wt, const __half* scales, const __half* zeros, __half* Y, int64_t ldy,
-                         uint8_t* ws, cudaStream_t st);
+                         uint8_t* ws, bool bf, cudaStream_t st);
 bool tcd_eligible(int64_t M, int32_t G);
 int splitk_grid(int work, int sms, bool expensive_partials);
 size_t tcd_workspace_bytes(int64_t M, int64_t N, int64_t K);
 tl_status tcd_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, const __half* A, int64_t lda,
                      const uint8_t* wt, const __half* scales, const __half* zeros, __half* Y, int64_t ldy,
-                     float* partial, int* sem, int grid_req, bool static_weights, cudaStream_t st);
+                     float* partial, int* sem, int grid_req, bool static_weights, bool bf, cudaStream_t st);
 
 }  // namespace tl

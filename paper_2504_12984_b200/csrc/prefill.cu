@@ -13,7 +13,7 @@ namespace tl {
 
 template <class F>
 tl_status launch_dq16(const uint8_t* wt, const __half* scales, const __half* zeros, __half* out, int N, int K, int G,
-                      int nt0, int ntiles, cudaStream_t st);
+                      int nt0, int ntiles, bool bf, cudaStream_t st);
 
 constexpr size_t kCublasWs = 32u << 20;     // cuBLAS workspace (set explicitly: no allocation, graph-capturable)
 constexpr size_t kChunkBytes = 64u << 20;   // decoded W^T chunk (stays in the 126 MB L2 for the GEMM)
@@ -34,7 +34,7 @@ static std::map<int, cublasHandle_t> g_cublas;
 
 tl_status prefill_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, const __half* A, int64_t lda,
                          const uint8_t* wt, const __half* scales, const __half* zeros, __half* Y, int64_t ldy,
-                         uint8_t* ws, cudaStream_t st) {
+                         uint8_t* ws, bool bf, cudaStream_t st) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return fail(TL_ECUDA, "cudaGetDevice failed");
   std::lock_guard<std::mutex> lk(g_cublas_mu);
@@ -57,13 +57,14 @@ tl_status prefill_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G,
     tl_status s = TL_EUNSUPPORTED;
     dispatch_format(w.kind, w.bits, w.kind == 2 ? w.exp_bits : 0, [&](auto f) {
       using F = decltype(f);
-      s = launch_dq16<F>(wt, scales, zeros, wbuf, (int)N, (int)K, G, (int)(n0 / kBN), (int)(nc / kBN), st);
+      s = launch_dq16<F>(wt, scales, zeros, wbuf, (int)N, (int)K, G, (int)(n0 / kBN), (int)(nc / kBN), bf, st);
     });
     if (s != TL_OK) return s;
     // Y^T[n0:n0+nc, :M] = (W^T chunk [nc, K]) x A^T  (column-major view of the row-major arrays)
-    const cublasStatus_t r = cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)nc, (int)M, (int)K, &alpha, wbuf,
-                                          CUDA_R_16F, (int)K, A, CUDA_R_16F, (int)lda, &beta, Y + n0, CUDA_R_16F,
-                                          (int)ldy, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+    const cudaDataType_t dt = bf ? CUDA_R_16BF : CUDA_R_16F;
+    const cublasStatus_t r = cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)nc, (int)M, (int)K, &alpha, wbuf, dt,
+                                          (int)K, A, dt, (int)lda, &beta, Y + n0, dt, (int)ldy, CUBLAS_COMPUTE_32F,
+                                          CUBLAS_GEMM_DEFAULT);
     if (r != CUBLAS_STATUS_SUCCESS) return fail(TL_ECUDA, "cublasGemmEx failed (%d)", (int)r);
   }
   return TL_OK;

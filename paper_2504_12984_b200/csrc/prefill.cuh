@@ -18,7 +18,7 @@
 namespace tl {
 
 // W^T[n0 + n, k] (row stride K) for the n-tiles [nt0, nt0 + ntiles) and every k-tile
-template <class F>
+template <class F, bool BF>
 __global__ void __launch_bounds__(128) dq16_kernel(const uint8_t* __restrict__ wt, const __half* __restrict__ scales,
                                                    const __half* __restrict__ zeros, __half* __restrict__ out,
                                                    int N, int K, int G, int nt0, uint32_t magic) {
@@ -46,11 +46,12 @@ __global__ void __launch_bounds__(128) dq16_kernel(const uint8_t* __restrict__ w
     const int64_t row = (int64_t)(kt * kBK + c * 32) / G;
     const uint32_t sb = __half_as_ushort(scales[row * N + col]);
     const __half2 s2 = u32_as_h2(sb | (sb << 16));
+    const float sf = Act<BF>::to_float(sb);
     uint32_t cp[10];
     if constexpr (F::kind != kFloat) {
       uint32_t zneg;
       if constexpr (F::kind == kUint) {
-        const uint32_t zb = (zeros ? (uint32_t)__half_as_ushort(zeros[row * N + col]) : 0u) ^ 0x8000u;
+        const uint32_t zb = zeros ? Act<BF>::neg_zero_h(__half_as_ushort(zeros[row * N + col])) : 0x8000u;
         zneg = zb | (zb << 16);
       } else {
         constexpr uint32_t zb = 0x8000u | ((uint32_t)(B - 1 + 15) << 10);  // -2^(b-1)
@@ -71,14 +72,22 @@ __global__ void __launch_bounds__(128) dq16_kernel(const uint8_t* __restrict__ w
     static_for<0, 16>([&](auto II) {
       constexpr int ii = decltype(II)::value;
       constexpr int i = (c & 1) * 16 + ii;
+      __half2 v;  // exact
       if constexpr (F::kind != kFloat) {
         constexpr int P = kPlan<F::kind, F::bits, F::exp>.pr[i].P;
         const uint32_t x = extract_pair<F, i>(bw, magic);
-        r[ii] = h2_as_u32(__hmul2(__hfma2(u32_as_h2(x), u32_as_h2(h2_pow2_neg<P>()), u32_as_h2(cp[P])), s2));
+        v = __hfma2(u32_as_h2(x), u32_as_h2(h2_pow2_neg<P>()), u32_as_h2(cp[P]));
       } else {
         constexpr uint32_t e = (uint32_t)(30 - F::bias) << 10;  // 2^(15-bias)
         const uint32_t x = extract_pair<F, i>(bw, 0u);
-        r[ii] = h2_as_u32(__hmul2(__hmul2(u32_as_h2(x), u32_as_h2(e | (e << 16))), s2));
+        v = __hmul2(u32_as_h2(x), u32_as_h2(e | (e << 16)));
+      }
+      if constexpr (!BF) {
+        r[ii] = h2_as_u32(__hmul2(v, s2));
+      } else {
+        const float2 f = __half22float2(v);
+        const __nv_bfloat162 b = __floats2bfloat162_rn(f.x * sf, f.y * sf);
+        r[ii] = *reinterpret_cast<const uint32_t*>(&b);
       }
     });
     uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
@@ -89,8 +98,9 @@ __global__ void __launch_bounds__(128) dq16_kernel(const uint8_t* __restrict__ w
 
 template <class F>
 tl_status launch_dq16(const uint8_t* wt, const __half* scales, const __half* zeros, __half* out, int N, int K, int G,
-                      int nt0, int ntiles, cudaStream_t st) {
-  dq16_kernel<F><<<ntiles * (K / kBK), 128, 0, st>>>(wt, scales, zeros, out, N, K, G, nt0, 0x64006400u);
+                      int nt0, int ntiles, bool bf, cudaStream_t st) {
+  if (bf) dq16_kernel<F, true><<<ntiles * (K / kBK), 128, 0, st>>>(wt, scales, zeros, out, N, K, G, nt0, 0x64006400u);
+  else dq16_kernel<F, false><<<ntiles * (K / kBK), 128, 0, st>>>(wt, scales, zeros, out, N, K, G, nt0, 0x64006400u);
   return check_launch("dq16_kernel");
 }
 

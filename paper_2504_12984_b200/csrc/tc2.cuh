@@ -46,6 +46,7 @@ struct Tc2Params {
   float* partial;  // [grid][2 slots][2 tiles][NB][128]
   int* sem;        // [n-pairs]
   uint32_t magic;  // 0x64006400 (a kernel argument: the LOP3 takes one immediate, see tcd)
+  int bf;          // 1: bf16 activations / scales / zeros / Y
   int dbg;         // TL_TC2_DBG timing experiments (results invalid): 1 skip partial stores, 2 skip reduction
 };
 
@@ -93,7 +94,7 @@ __host__ __device__ constexpr bool tc2_plan_uses_p(int P) {
 //   ints:   LOP3(s) -> 1024 + u*2^P (magic form); HFMA2(x, 2^-P, -(2^(10-P) + z)) = u - z exactly;
 //           HMUL2 by s (one fp16 rounding, reading R9)
 //   floats: LOP3(s) -> value(code) * 2^(bias-15) exactly; HMUL2 by 2^(15-bias) (exact), HMUL2 by s
-template <class F, bool kSubG>
+template <class F, bool kSubG, bool BF>
 __device__ __forceinline__ void tc2_dequant_tile(uint32_t wtile, int n, uint32_t tslot, uint32_t magic,
                                                  const uint32_t (&sc)[4], const uint32_t (&zc)[4]) {
   constexpr int B = F::bits;
@@ -112,7 +113,7 @@ __device__ __forceinline__ void tc2_dequant_tile(uint32_t wtile, int n, uint32_t
     if constexpr (F::kind != kFloat) {
       uint32_t zneg;
       if constexpr (F::kind == kUint) {
-        const uint32_t zb = zc[c] ^ 0x8000u;
+        const uint32_t zb = Act<BF>::neg_zero_h(zc[c]);
         zneg = zb | (zb << 16);
       } else {
         constexpr uint32_t zb = 0x8000u | ((uint32_t)(B - 1 + 15) << 10);  // -2^(b-1)
@@ -134,27 +135,35 @@ __device__ __forceinline__ void tc2_dequant_tile(uint32_t wtile, int n, uint32_t
     uint32_t bw[2 * B];
 #pragma unroll
     for (int j = 0; j < 2 * B; ++j) bw[j] = words[tile_word(h, j)];
-    const __half2 s2 = u32_as_h2(sc[cs] | (sc[cs] << 16));
+    const __half2 s2 = u32_as_h2(sc[cs] | (sc[cs] << 16));  // fp16 activations
+    const float sf = Act<BF>::to_float(sc[cs]);              // bf16 activations
     uint32_t r[16];
     static_for<0, 16>([&](auto II) {
       constexpr int ii = decltype(II)::value;
       constexpr int i = (c & 1) * 16 + ii;  // pair within the block
+      __half2 v;                             // exact: u - z, or value(code) (floats)
       if constexpr (F::kind != kFloat) {
         constexpr int P = kPlan<F::kind, F::bits, F::exp>.pr[i].P;
         const uint32_t x = extract_pair<F, i>(bw, magic);
-        const __half2 v = __hfma2(u32_as_h2(x), u32_as_h2(h2_pow2_neg<P>()), u32_as_h2(cp[cs][P]));
-        r[ii] = h2_as_u32(__hmul2(v, s2));
+        v = __hfma2(u32_as_h2(x), u32_as_h2(h2_pow2_neg<P>()), u32_as_h2(cp[cs][P]));
       } else {
         constexpr uint32_t e = (uint32_t)(30 - F::bias) << 10;  // fp16 bits of 2^(15-bias)
         const uint32_t x = extract_pair<F, i>(bw, 0u);
-        r[ii] = h2_as_u32(__hmul2(__hmul2(u32_as_h2(x), u32_as_h2(e | (e << 16))), s2));
+        v = __hmul2(u32_as_h2(x), u32_as_h2(e | (e << 16)));
+      }
+      if constexpr (!BF) {
+        r[ii] = h2_as_u32(__hmul2(v, s2));  // one fp16 rounding (reading R9)
+      } else {
+        const float2 f = __half22float2(v);   // exact; then one bf16 rounding of value * s
+        const __nv_bfloat162 b = __floats2bfloat162_rn(f.x * sf, f.y * sf);
+        r[ii] = *reinterpret_cast<const uint32_t*>(&b);
       }
     });
     tc2_tmem_st16(tslot + c * 16, r);
   });
 }
 
-template <class F, bool kSubG>
+template <class F, bool kSubG, bool BF>
 __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_constant__ CUtensorMap tmapA, Tc2Params p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -234,7 +243,8 @@ __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_consta
   } else if (warp == 1) {
     // ------------------------------ MMA issuer (one thread) ------------------------------
     if (elect_one()) {
-      const uint32_t idesc = (1u << 4) | ((uint32_t)(NB >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+      const uint32_t idesc =
+          (1u << 4) | Act<BF>::idesc_ab | ((uint32_t)(NB >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
       const uint32_t bblk = (uint32_t)NB * 8;  // NB*128 B in 16-B descriptor units
       int s = 0, ph = 0, np = u0 / KT, kt = u0 - (u0 / KT) * KT, seg = 0;
       bool first = true;
@@ -336,8 +346,8 @@ __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_consta
         mbar_wait(&full_tma[s], (t / NS) & 1);
         if (kk >= 1) mbar_wait(&empty_w[g], (kk - 1) & 1);  // MMA of this group's previous unit done
         const uint32_t wst = st_u + s * SB + p.w_off_in_stage;
-        tc2_dequant_tile<F, kSubG>(wst, n, tmem + lane_off + g * 128, p.magic, sc[0], zc[0]);
-        if (two) tc2_dequant_tile<F, kSubG>(wst + WB, n, tmem + lane_off + g * 128 + 64, p.magic, sc[1], zc[1]);
+        tc2_dequant_tile<F, kSubG, BF>(wst, n, tmem + lane_off + g * 128, p.magic, sc[0], zc[0]);
+        if (two) tc2_dequant_tile<F, kSubG, BF>(wst + WB, n, tmem + lane_off + g * 128 + 64, p.magic, sc[1], zc[1]);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
@@ -366,7 +376,7 @@ __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_consta
             const int m = cb + j;
             if (m < p.M) {
               const float v = __uint_as_float(r[j]);
-              if (complete) p.Y[(int64_t)m * p.ldy + col] = __float2half_rn(v);
+              if (complete) reinterpret_cast<unsigned short*>(p.Y)[(int64_t)m * p.ldy + col] = Act<BF>::from_float(v);
               else if (!(p.dbg & 1)) __stcg(part + (int64_t)m * kBN + n, v);
             }
           }
@@ -433,8 +443,9 @@ __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_consta
                 const int e = e0 + j * kTc2Groups * 128;
                 if (e < nv) {
                   const int m = e >> 5, c4 = e & 31;  // kBN / 4 == 32 float4 per row
-                  const uint2 o = make_uint2(h2_as_u32(__floats2half2_rn(acc[j].x, acc[j].y)),
-                                             h2_as_u32(__floats2half2_rn(acc[j].z, acc[j].w)));
+                  const uint2 o = make_uint2(
+                      (uint32_t)Act<BF>::from_float(acc[j].x) | ((uint32_t)Act<BF>::from_float(acc[j].y) << 16),
+                      (uint32_t)Act<BF>::from_float(acc[j].z) | ((uint32_t)Act<BF>::from_float(acc[j].w) << 16));
                   *reinterpret_cast<uint2*>(p.Y + (int64_t)m * p.ldy + (2 * np + tj) * kBN + 4 * c4) = o;
                 }
               }
@@ -455,15 +466,16 @@ __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_consta
 
 template <class F>
 tl_status launch_tc2(const Tc2Params& p, const CUtensorMap* tmap, int grid, uint32_t smem_bytes, cudaStream_t st) {
-  if (p.G < kBK) {
-    if (prepare_kernel(reinterpret_cast<const void*>(tc2_kernel<F, true>), 227 * 1024, kTc2Threads) == 0)
+  auto go = [&](auto kern) -> tl_status {
+    if (prepare_kernel(reinterpret_cast<const void*>(kern), 227 * 1024, kTc2Threads) == 0)
       return fail(TL_ECUDA, "tc2_kernel: %s", tl_last_error());
-    tc2_kernel<F, true><<<grid, kTc2Threads, smem_bytes, st>>>(*tmap, p);
-  } else {
-    if (prepare_kernel(reinterpret_cast<const void*>(tc2_kernel<F, false>), 227 * 1024, kTc2Threads) == 0)
-      return fail(TL_ECUDA, "tc2_kernel: %s", tl_last_error());
-    tc2_kernel<F, false><<<grid, kTc2Threads, smem_bytes, st>>>(*tmap, p);
-  }
+    kern<<<grid, kTc2Threads, smem_bytes, st>>>(*tmap, p);
+    return TL_OK;
+  };
+  tl_status r;
+  if (p.G < kBK) r = p.bf ? go(tc2_kernel<F, true, true>) : go(tc2_kernel<F, true, false>);
+  else r = p.bf ? go(tc2_kernel<F, false, true>) : go(tc2_kernel<F, false, false>);
+  if (r != TL_OK) return r;
   return check_launch("tc2_kernel");
 }
 

@@ -47,6 +47,7 @@ struct TcdParams {
   uint32_t stage_bytes;            // [R weight tiles | R scale row slices | R zero row slices]
   uint32_t stash_off;              // decode: A[0, 0:K] resident in shared memory (K*2 bytes)
   int rot;                         // 1: decode configuration TcdCfg<1> (M = 1, K*2 <= 64 KB)
+  int bf;                          // 1: bf16 activations / scales / zeros / Y (Act<true>)
   uint32_t op_off, red_off, bar_off;  // operand ring [NOP][4 KB] (1024-aligned), reduction, barriers
   const uint8_t* wt;
   const __half* A;
@@ -186,7 +187,7 @@ __device__ __forceinline__ void tcd_istamp(const TcdParams& p, int dw, int lane,
 // full HBM rate only with stages of ~12 KB and more, tools/tma_probe.cu)
 __host__ __device__ constexpr int tcd_tiles_per_stage(int b) { return (6 + b - 1) / b; }
 
-template <class F, int MT>
+template <class F, int MT, bool BF>
 __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_constant__ CUtensorMap tmapA, TcdParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -368,7 +369,8 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
     // the dequant group has already seen the tile's activation operand land (full_op) before it
     // arrives on full_w, so the issuer waits only for the W^T slot and the accumulator
     if (elect_one()) {
-      const uint32_t idesc = (1u << 4) | ((uint32_t)(kTcdNB >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+      const uint32_t idesc =
+          (1u << 4) | Act<BF>::idesc_ab | ((uint32_t)(kTcdNB >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
       int o = 0, g = 0, a = 0;
       uint32_t kk = 0, ka = 0;  // t / NW, t / NACC
       for (int t = 0; t < T; ++t) {
@@ -496,13 +498,13 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
         const uint32_t st = st_u + s * SB;
         uint32_t words[4 * F::bits];
         tcd_load_words<F::bits>(st + jt * WB, n, words);
-        const float sc = __half2float(__ushort_as_half(lds16(st + kR * WB + 256 * jt + 2 * n)));
+        const float sc = Act<BF>::to_float(lds16(st + kR * WB + 256 * jt + 2 * n));
         // ints: -z as fp16x2 (zero point of the tile's group; offset-binary ints: 2^(b-1))
         uint32_t zneg = 0;
         if constexpr (kInt) {
           if constexpr (F::kind == kUint) {
             if (has_zeros) {
-              const uint32_t zb = (uint32_t)lds16(st + kR * WB + kR * 256 + 256 * jt + 2 * n) ^ 0x8000u;
+              const uint32_t zb = Act<BF>::neg_zero_h(lds16(st + kR * WB + kR * 256 + 256 * jt + 2 * n));
               zneg = zb | (zb << 16);
             }
           } else {
@@ -535,10 +537,10 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
             if constexpr (kInt) {
               constexpr int P = kPlan<F::kind, F::bits, F::exp>.pr[i].P;
               const uint32_t x = extract_pair<F, i>(bw, p.magic);
-              r[decltype(II)::value] =
-                  h2_as_u32(__hfma2(u32_as_h2(x), u32_as_h2(h2_pow2_neg<P>()), u32_as_h2(cp[P])));
+              r[decltype(II)::value] = Act<BF>::from_h2(
+                  h2_as_u32(__hfma2(u32_as_h2(x), u32_as_h2(h2_pow2_neg<P>()), u32_as_h2(cp[P]))));
             } else {
-              r[decltype(II)::value] = extract_pair<F, i>(bw, 0u);
+              r[decltype(II)::value] = Act<BF>::from_h2(extract_pair<F, i>(bw, 0u));
             }
           });
         };
@@ -612,7 +614,7 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
         float v = 0.f;
 #pragma unroll
         for (int gg = 0; gg < NG; ++gg) v += red[(gg * p.M + m) * kBN + n];
-        if (complete) p.Y[(int64_t)m * p.ldy + col] = __float2half_rn(v);
+        if (complete) reinterpret_cast<unsigned short*>(p.Y)[(int64_t)m * p.ldy + col] = Act<BF>::from_float(v);
         else __stcg(part + (int64_t)m * kBN + n, v);
       }
       if (!complete) {
@@ -635,7 +637,7 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
           const int lo = flag[1], hi = flag[2];
           for (int m = g; m < p.M; m += NG) {
             const float sum = streamk_sum(p.partial, lo, hi, flag[3], (int64_t)kTcdNB * kBN, (int64_t)m * kBN + n);
-            p.Y[(int64_t)m * p.ldy + col] = __float2half_rn(sum);
+            reinterpret_cast<unsigned short*>(p.Y)[(int64_t)m * p.ldy + col] = Act<BF>::from_float(sum);
           }
           if (threadIdx.x == 128) p.sem[nt] = 0;
         }
@@ -653,9 +655,9 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
   if (threadIdx.x == 0) tcd_stamp(p, 7);
 }
 
-template <class F, int MT>
+template <class F, int MT, bool BF>
 tl_status launch_tcd_mt(const TcdParams& p, const CUtensorMap* tmap, int grid, uint32_t smem_bytes, cudaStream_t st) {
-  if (prepare_kernel(reinterpret_cast<const void*>(tcd_kernel<F, MT>), 227 * 1024, kTcdThreads) == 0)
+  if (prepare_kernel(reinterpret_cast<const void*>(tcd_kernel<F, MT, BF>), 227 * 1024, kTcdThreads) == 0)
     return fail(TL_ECUDA, "tcd_kernel: %s", tl_last_error());
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -667,15 +669,17 @@ tl_status launch_tcd_mt(const TcdParams& p, const CUtensorMap* tmap, int grid, u
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = (p.dbg & 128) ? 0 : 1;  // TL_TCD_DBG=128: plain stream order (A/B of the PDL overlap)
-  cudaError_t e = cudaLaunchKernelEx(&cfg, tcd_kernel<F, MT>, *tmap, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tcd_kernel<F, MT, BF>, *tmap, p);
   if (e != cudaSuccess) return fail(TL_ECUDA, "tcd_kernel launch: %s", cudaGetErrorString(e));
   return check_launch("tcd_kernel");
 }
 
 template <class F>
 tl_status launch_tcd(const TcdParams& p, const CUtensorMap* tmap, int grid, uint32_t smem_bytes, cudaStream_t st) {
-  return p.rot ? launch_tcd_mt<F, 1>(p, tmap, grid, smem_bytes, st)
-               : launch_tcd_mt<F, kTcdNB>(p, tmap, grid, smem_bytes, st);
+  if (p.bf) return p.rot ? launch_tcd_mt<F, 1, true>(p, tmap, grid, smem_bytes, st)
+                       : launch_tcd_mt<F, kTcdNB, true>(p, tmap, grid, smem_bytes, st);
+  return p.rot ? launch_tcd_mt<F, 1, false>(p, tmap, grid, smem_bytes, st)
+               : launch_tcd_mt<F, kTcdNB, false>(p, tmap, grid, smem_bytes, st);
 }
 
 }  // namespace tl

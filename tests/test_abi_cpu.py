@@ -81,10 +81,11 @@ def test_bad_arguments_rejected_before_any_launch(lib):
     st = lib._lib._tl_matmul(w, 0, 1, 128, 128, 128, 16, 128, 16, 16, None, 16, 128, 16, 64, None)
     assert lib._lib._tl_status_str(st).decode() == "TL_EWORKSPACE"
     assert "workspace" in lib._lib._tl_last_error().decode()
-    # bf16 activations are reserved: rejected, and no workspace size is defined
-    st = lib._lib._tl_matmul(w, 1, 1, 128, 128, 128, 16, 128, 16, 16, None, 16, 128, 16, 1 << 24, None)
+    # activation types: fp16 and bf16 are defined, anything else is rejected
+    st = lib._lib._tl_matmul(w, 7, 1, 128, 128, 128, 16, 128, 16, 16, None, 16, 128, 16, 1 << 24, None)
     assert lib._lib._tl_status_str(st).decode() == "TL_EUNSUPPORTED"
-    assert lib.tl_matmul_workspace_bytes(w, 1, 128, 128, 128, atype=lib.TL_ACT_BF16) == 0
+    assert lib.tl_matmul_workspace_bytes(w, 1, 128, 128, 128, atype=7) == 0
+    assert lib.tl_matmul_workspace_bytes(w, 1, 128, 128, 128, atype=lib.TL_ACT_BF16) > 0
     # tl_matmul_ex: unknown flags / paths, negative splits
     def ex(path=0, splits=0, flags=0):
         return lib._lib._tl_status_str(lib._lib._tl_matmul_ex(w, 0, 1, 128, 128, 128, 16, 128, 16, 16, None, 16,
