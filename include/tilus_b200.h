@@ -60,7 +60,13 @@ typedef struct {
  * tensor-core families (decode, batched, prefill); a TL_PATH_GEMV request with bf16 runs on the
  * decode / batched tensor-core kernel instead.  The dequantized weight is exact in fp16 and is
  * rounded once to bf16 where the MMA / GEMM operand is bf16 (reading R9). */
-typedef enum { TL_ACT_F16 = 0, TL_ACT_BF16 = 1 } tl_atype;
+/* TL_ACT_I8 ("operand A can have data types with 32, 16, or 8 bits",
+ * PAPER.md:527 "we also support ... int8"; reading R24): A is int8 [M,K] (lda in elements = bytes,
+ * a multiple of 16); scales, zeros and Y are fp16.  Each int8 is the integer it encodes, so the
+ * result is the same definition Y = fp16(sum_k A[m,k] * w[k,n]).  The library stages A exactly as
+ * fp16 in the tail of the workspace (tl_matmul_workspace_bytes(.., TL_ACT_I8, ..) includes it) and
+ * runs the fp16 families on the copy. */
+typedef enum { TL_ACT_F16 = 0, TL_ACT_BF16 = 1, TL_ACT_I8 = 2 } tl_atype;
 
 typedef enum {
   TL_OK = 0,
@@ -149,7 +155,7 @@ size_t tl_matmul_workspace_bytes(tl_wtype w, tl_atype a, int64_t M, int64_t N, i
 
 /* Y[M,N] (row stride ldy elements) = A[M,K] (row stride lda elements) x dequant(w_t): the paper's
  * C = A x B with fp32 accumulation cast to the activation type.
- * A, scales and Y have type `a`.  scales: [K/G, N] row-major.  zeros: [K/G, N] with integer
+ * A, scales and Y have type `a` (for TL_ACT_I8: A int8, scales / zeros / Y fp16).  scales: [K/G, N] row-major.  zeros: [K/G, N] with integer
  * values, uint formats only, or NULL (z = 0).  Enqueued on `stream`; no flags: every read is
  * ordered after the previous kernel in the stream. */
 tl_status tl_matmul(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group, const void* A,
@@ -178,6 +184,51 @@ tl_status tl_matmul_hostio(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t
  * sweep).  The rule is DESIGN.md "Dispatch". */
 tl_status tl_matmul_plan(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group,
                          int32_t* path_out, int32_t* splits_out);
+
+/* ---- row f3: gathered output over NVLink peer memory --------------------------------------------- */
+
+/* Column-sharded matmul with the all-gather FUSED into the epilogue (north star
+ * (5); output column n depends only on W[:, n], so a column shard computes alone).
+ * Rank r owns columns [n0, n1) of an [M, N_total] layer; every rank holds a gathered buffer
+ * Yg[M, N_total] (row stride ldy) and a flag array flags[nranks] (uint32, zero-initialised, never
+ * reset).  This call computes the rank's shard exactly like tl_matmul (A, w_t, scales, zeros are the
+ * shard's; N = n1 - n0) into Y = &Yg_local[0, n0], and the kernel's epilogue also stores every
+ * finished element into each peer's gathered buffer: Y_peers[i] = device address, mapped into this
+ * process (CUDA IPC / peer access over NVLink), of &Yg_peer_i[0, n0] with the same ldy.  When the
+ * last element is stored, the kernel releases +1 (system scope) on flag_peers[i] = &flags_peer_i[r].
+ * The fused epilogue runs in the decode and batched tensor-core kernels; the other families compute
+ * locally and then replicate with one copy-and-signal kernel.  Y_peers / flag_peers are HOST arrays
+ * of npeers <= 7 device pointers (npeers = 0: a plain tl_matmul).  Ordering contract: the caller
+ * must not start call e+1 into a peer's buffer before that peer has consumed call e (alternate two
+ * gathered buffers, or rely on the layer dependency).  M == 0 sends and signals nothing.  Errors as
+ * tl_matmul_ex, plus TL_EINVAL_SHAPE for npeers outside [0, 7], TL_ENULL / TL_EALIGN for peer
+ * pointers (Y 16-byte, flag 4-byte aligned). */
+tl_status tl_matmul_gathered(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group,
+                             const void* A, int64_t lda, const void* w_t, const void* scales,
+                             const void* zeros, void* Y, int64_t ldy, void* const* Y_peers,
+                             uint32_t* const* flag_peers, int32_t npeers, void* workspace,
+                             size_t workspace_bytes, uint32_t flags, void* stream);
+
+/* Consumer side of tl_matmul_gathered: enqueue on `stream` a wait until every other rank q != self
+ * has completed `epoch` gathered calls into this rank (flags[q] >= epoch, wrap-safe; flags is this
+ * rank's own device array [nranks]).  Kernels enqueued after it on `stream` see the peers' stores.
+ * The wait is bounded (TL_GATHER_TIMEOUT_MS, default 10000): a peer that never arrives makes the
+ * wait kernel trap (a CUDA launch failure at the next synchronisation) instead of hanging.
+ * TL_EINVAL_SHAPE unless 1 <= nranks <= 8 and 0 <= self < nranks; TL_ENULL for NULL flags. */
+tl_status tl_gather_wait(const uint32_t* flags, int32_t nranks, int32_t self, uint32_t epoch, void* stream);
+
+/* Microscaling scales ("Microscaling data types can be thought as
+ * a more fine-grained quantization thus we could also support it"; reading R25).  An MX weight is a
+ * kernel format (fp4 e2m1, fp6 e2m3 / e3m2, fp8 e4m3, or int8 for MXINT8) with ONE E8M0 scale per
+ * block of 32 weights along K: pass group = 32 to tl_matmul with the fp16 scales this call writes.
+ * e8m0[count] (device, any layout -- conventionally [K/32, N]) holds exponent codes e; scales_f16
+ * [count] (device) receives 2^(e - 127 + exp_adjust) as fp16 (exp_adjust = -6 for MXINT8, whose
+ * elements carry an implicit 2^-6; 0 otherwise).  Exact whenever the value is an fp16 number
+ * (2^-24 .. 2^15); outside that range, and for the E8M0 NaN code 0xFF, the scale is an fp16 NaN (the
+ * block's outputs become NaN rather than silently wrong).  One-time weight preparation, enqueued on
+ * `stream`.  TL_EINVAL_SHAPE for count < 0 or |exp_adjust| > 64, TL_ENULL for NULL pointers. */
+tl_status tl_mx_scales_to_f16(const uint8_t* e8m0, int64_t count, int32_t exp_adjust, void* scales_f16,
+                              void* stream);
 
 /* Test hook: out[K,N] fp32 = (value(q) - z) * s, computed exactly in fp32 from
  * the TRANSFORMED weight (reading R9: exact, so it is bit-comparable with the

@@ -21,6 +21,7 @@ Modules
   matmul   -- O6/O7: fp64 matmul C = A x B and the tolerance
               comparator the north star states
   quantize -- O9: round-to-nearest-even encoder used only to build test data
+  mx       -- row f4: E8M0 microscaling block scales and MX dequant (reading R25)
 
 Every function here is pinned by a ``-m "not gpu"`` test in
 ``tests/test_oracle_*.py`` against something other than itself (ml_dtypes
@@ -33,9 +34,10 @@ from .packing import pack, unpack, packed_nbytes
 from .dequant import dequant
 from .matmul import matmul_fp64, matmul_cols_fp64, tolerance_check
 from .quantize import encode
+from .mx import e8m0_value, e8m0_to_f16_scale, mx_dequant, MX_BLOCK
 
 __all__ = [
     "WType", "parse_wtype", "all_kernel_formats", "oracle_only_formats", "code_values",
     "pack", "unpack", "packed_nbytes", "dequant", "matmul_fp64", "matmul_cols_fp64",
-    "tolerance_check", "encode",
+    "tolerance_check", "encode", "e8m0_value", "e8m0_to_f16_scale", "mx_dequant", "MX_BLOCK",
 ]

@@ -54,7 +54,7 @@ def wtype(name: str) -> tl_wtype:
 
 
 TL_PATH_AUTO, TL_PATH_GEMV, TL_PATH_TC, TL_PATH_TCD, TL_PATH_PREFILL = 0, 1, 2, 3, 4
-TL_ACT_F16, TL_ACT_BF16 = 0, 1
+TL_ACT_F16, TL_ACT_BF16, TL_ACT_I8 = 0, 1, 2
 TL_FLAG_STATIC_WEIGHTS = 1
 
 _c_size = ctypes.c_size_t
@@ -91,13 +91,18 @@ _tl_matmul_hostio = _sig("tl_matmul_hostio", ctypes.c_int,
                           _vp])
 _tl_matmul_plan = _sig("tl_matmul_plan", ctypes.c_int,
                        [_W, _A, _i64, _i64, _i64, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32)])
+_tl_matmul_gathered = _sig("tl_matmul_gathered", ctypes.c_int,
+                           [_W, _A, _i64, _i64, _i64, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _i64,
+                            ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i32, _vp, _c_size, _u32, _vp])
+_tl_gather_wait = _sig("tl_gather_wait", ctypes.c_int, [_vp, _i32, _i32, _u32, _vp])
+_tl_mx_scales_to_f16 = _sig("tl_mx_scales_to_f16", ctypes.c_int, [_vp, _i64, _i32, _vp, _vp])
 _tl_dequant = _sig("tl_dequant", ctypes.c_int, [_W, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _vp])
 _tl_status_str = _sig("tl_status_str", ctypes.c_char_p, [ctypes.c_int])
 _tl_last_error = _sig("tl_last_error", ctypes.c_char_p, [])
 
 EXPORTED = ["tl_packed_bytes", "tl_transformed_bytes", "tl_format_version", "tl_pack", "tl_unpack",
             "tl_transform_weights", "tl_untransform_weights", "tl_matmul_workspace_bytes", "tl_matmul",
-            "tl_matmul_ex", "tl_matmul_hostio", "tl_matmul_plan", "tl_dequant", "tl_status_str",
+            "tl_matmul_ex", "tl_matmul_hostio", "tl_matmul_plan", "tl_matmul_gathered", "tl_gather_wait", "tl_mx_scales_to_f16", "tl_dequant", "tl_status_str",
             "tl_last_error"]
 
 
@@ -187,9 +192,44 @@ def tl_dequant(w: tl_wtype, K: int, N: int, group: int, w_t: torch.Tensor, scale
 
 
 # ---- the hot path ---------------------------------------------------------------------------
-def alloc_workspace(w: tl_wtype, M: int, N: int, K: int, group: int, device="cuda") -> torch.Tensor:
+def alloc_workspace(w: tl_wtype, M: int, N: int, K: int, group: int, device="cuda",
+                    atype: int = TL_ACT_F16) -> torch.Tensor:
     """Zero-filled workspace (the kernels keep its semaphores at zero between calls)."""
-    return torch.zeros(tl_matmul_workspace_bytes(w, M, N, K, group), dtype=torch.uint8, device=device)
+    return torch.zeros(tl_matmul_workspace_bytes(w, M, N, K, group, atype), dtype=torch.uint8, device=device)
+
+
+def tl_matmul_gathered(w: tl_wtype, M: int, N: int, K: int, group: int, A: torch.Tensor, w_t: torch.Tensor,
+                       scales: torch.Tensor, zeros: torch.Tensor | None, Y: torch.Tensor, ldy: int,
+                       Y_peers: list[int], flag_peers: list[int], workspace: torch.Tensor, lda: int | None = None,
+                       flags: int = 0, stream=None) -> None:
+    """Row f3.  Y: a view whose data_ptr is &Yg_local[0, n0] (row stride ldy); Y_peers / flag_peers:
+    integer device addresses (peer-mapped) of &Yg_peer[0, n0] and &flags_peer[rank]."""
+    n = len(Y_peers)
+    if len(flag_peers) != n:
+        raise ValueError("Y_peers and flag_peers differ in length")
+    yp = (_vp * max(n, 1))(*Y_peers)
+    fp = (_vp * max(n, 1))(*flag_peers)
+    _check(_tl_matmul_gathered(w, _atype(A), M, N, K, group, _ptr(A), lda if lda is not None else K, _ptr(w_t),
+                               _ptr(scales), _ptr(zeros), Y.data_ptr(), ldy, yp, fp, n, _ptr(workspace),
+                               workspace.numel(), flags, _stream(stream)), "tl_matmul_gathered")
+
+
+def tl_gather_wait(flags: torch.Tensor, nranks: int, rank: int, epoch: int, stream=None) -> None:
+    """Row f3: enqueue the wait for every other rank's `epoch`-th gathered call into this rank."""
+    if flags.dtype not in (torch.int32, torch.uint32) or flags.numel() < nranks:
+        raise ValueError("flags must be an int32/uint32 device tensor with nranks entries")
+    _check(_tl_gather_wait(_ptr(flags), nranks, rank, epoch & 0xFFFFFFFF, _stream(stream)), "tl_gather_wait")
+
+
+def tl_mx_scales_to_f16(e8m0: torch.Tensor, exp_adjust: int = 0, out: torch.Tensor | None = None,
+                        stream=None) -> torch.Tensor:
+    """E8M0 block-scale codes (uint8, any shape) -> fp16 scales 2^(e-127+exp_adjust) (NaN if not fp16)."""
+    if e8m0.dtype != torch.uint8:
+        raise ValueError("e8m0 must be uint8")
+    out = out if out is not None else torch.empty(e8m0.shape, dtype=torch.float16, device=e8m0.device)
+    _check(_tl_mx_scales_to_f16(_ptr(e8m0), e8m0.numel(), exp_adjust, _ptr(out), _stream(stream)),
+           "tl_mx_scales_to_f16")
+    return out
 
 
 def _atype(A: torch.Tensor) -> int:
@@ -197,7 +237,9 @@ def _atype(A: torch.Tensor) -> int:
         return TL_ACT_F16
     if A.dtype == torch.bfloat16:
         return TL_ACT_BF16
-    raise ValueError(f"activations must be fp16 or bf16, got {A.dtype}")
+    if A.dtype == torch.int8:
+        return TL_ACT_I8
+    raise ValueError(f"activations must be fp16, bf16 or int8, got {A.dtype}")
 
 
 def tl_matmul(w: tl_wtype, M: int, N: int, K: int, group: int, A: torch.Tensor, w_t: torch.Tensor,

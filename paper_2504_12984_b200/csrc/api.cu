@@ -104,6 +104,11 @@ const char* tl_status_str(tl_status s) {
 const char* tl_last_error(void) { return g_err; }
 
 size_t tl_matmul_workspace_bytes(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group) {
+  if (a == TL_ACT_I8) {
+    // row f4: the fp16 workspace, then the exact fp16 copy of A (act8.cu)
+    const size_t f16 = tl_matmul_workspace_bytes(w, TL_ACT_F16, M, N, K, group);
+    return M > 0 && K > 0 ? a8_staging_offset(f16) + (size_t)M * (size_t)K * 2 : f16;
+  }
   (void)w;
   (void)group;
   if (a != TL_ACT_F16 && a != TL_ACT_BF16) return 0;
@@ -121,6 +126,7 @@ size_t tl_matmul_workspace_bytes(tl_wtype w, tl_atype a, int64_t M, int64_t N, i
 
 tl_status tl_matmul_plan(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group,
                          int32_t* path_out, int32_t* splits_out) {
+  if (a == TL_ACT_I8) a = TL_ACT_F16;  // int8 activations run the fp16 families on the staged copy
   if (a != TL_ACT_F16 && a != TL_ACT_BF16) return fail(TL_EUNSUPPORTED, "unknown activation type %d", (int)a);
   (void)K;
   int path = choose_path(w, M, N, group);
@@ -138,13 +144,18 @@ tl_status tl_matmul_plan(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K
   return TL_OK;
 }
 
-tl_status tl_matmul_ex(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group, const void* A,
-                       int64_t lda, const void* w_t, const void* scales, const void* zeros, void* Y, int64_t ldy,
-                       void* workspace, size_t workspace_bytes, int32_t path, int32_t splits, uint32_t flags,
-                       void* stream) {
+}  // extern "C"
+
+// The body of tl_matmul_ex; `po` (row f3, peer.cuh) non-NULL = gathered output: every finished
+// element of Y is also stored into the peers' gathered buffers and the peers are signalled.
+static tl_status matmul_core(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group, const void* A,
+                             int64_t lda, const void* w_t, const void* scales, const void* zeros, void* Y, int64_t ldy,
+                             void* workspace, size_t workspace_bytes, int32_t path, int32_t splits, uint32_t flags,
+                             const PeerOut* po, void* stream) {
   tl_status st;
   if ((st = check_wtype(w)) != TL_OK) return st;
-  if (a != TL_ACT_F16 && a != TL_ACT_BF16) return fail(TL_EUNSUPPORTED, "unknown activation type %d", (int)a);
+  if (a != TL_ACT_F16 && a != TL_ACT_BF16 && a != TL_ACT_I8)
+    return fail(TL_EUNSUPPORTED, "unknown activation type %d", (int)a);
   const bool bf = a == TL_ACT_BF16;
   if (flags & ~TL_FLAG_STATIC_WEIGHTS) return fail(TL_EINVAL_SHAPE, "unknown flags 0x%x", flags);
   if (path < TL_PATH_AUTO || path > TL_PATH_PREFILL) return fail(TL_EUNSUPPORTED, "unknown path %d", path);
@@ -157,17 +168,33 @@ tl_status tl_matmul_ex(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, 
   if (!A || !w_t || !scales || !Y) return fail(TL_ENULL, "tl_matmul: NULL pointer");
   if (zeros && w.kind != 0) return fail(TL_EZEROS, "zero points are for uint formats only (reading R6)");
   if (lda < K || ldy < N) return fail(TL_EINVAL_SHAPE, "lda=%lld < K or ldy=%lld < N", (long long)lda, (long long)ldy);
+  const int64_t a_esize = a == TL_ACT_I8 ? 1 : 2;
   if (!aligned16(A) || !aligned16(w_t) || !aligned16(scales) || !aligned16(Y) || (zeros && !aligned16(zeros)) ||
-      (lda * 2) % 16 || (ldy * 2) % 16)
+      (lda * a_esize) % 16 || (ldy * 2) % 16)
     return fail(TL_EALIGN, "pointers and row strides must be 16-byte aligned");
   const size_t need = tl_matmul_workspace_bytes(w, a, M, N, K, group);
   if (!workspace || workspace_bytes < need)
     return fail(TL_EWORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
   if (!aligned16(workspace)) return fail(TL_EALIGN, "workspace must be 16-byte aligned");
+  if (a == TL_ACT_I8) {
+    // row f4 (reading R24): stage A exactly as fp16 behind the fp16 workspace, then the fp16 path
+    const size_t f16 = tl_matmul_workspace_bytes(w, TL_ACT_F16, M, N, K, group);
+    __half* staged = reinterpret_cast<__half*>(reinterpret_cast<uint8_t*>(workspace) + a8_staging_offset(f16));
+    if ((st = stage_a8(reinterpret_cast<const int8_t*>(A), lda, M, K, staged, as_stream(stream))) != TL_OK) return st;
+    return matmul_core(w, TL_ACT_F16, M, N, K, group, staged, K, w_t, scales, zeros, Y, ldy, workspace,
+                       a8_staging_offset(f16), path, splits, flags, po, stream);
+  }
   if (path == TL_PATH_AUTO) path = choose_path(w, M, N, group);
   // the CUDA-core kernels are fp16-only: bf16 requests run on the tensor-core families
   if (bf && path == TL_PATH_GEMV) path = tcd_eligible(M, group) ? TL_PATH_TCD : TL_PATH_TC;
   if (path == TL_PATH_TCD && !tcd_eligible(M, group)) path = TL_PATH_TC;
+  if (po && path != TL_PATH_TCD && path != TL_PATH_TC) {
+    // families without a fused epilogue: the local result, then one replicate-and-signal kernel
+    st = matmul_core(w, a, M, N, K, group, A, lda, w_t, scales, zeros, Y, ldy, workspace, workspace_bytes, path,
+                     splits, flags, nullptr, stream);
+    if (st != TL_OK) return st;
+    return gather_push(*po, reinterpret_cast<const __half*>(Y), ldy, M, N, as_stream(stream));
+  }
   int* sem = reinterpret_cast<int*>(workspace);
   float* partial = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(workspace) + kSemBytes);
   cudaStream_t s = as_stream(stream);
@@ -221,7 +248,7 @@ tl_status tl_matmul_ex(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, 
     tl_status r = tcd_matmul(w, M, N, K, group, reinterpret_cast<const __half*>(A), lda,
                              reinterpret_cast<const uint8_t*>(w_t), reinterpret_cast<const __half*>(scales),
                              reinterpret_cast<const __half*>(zeros), reinterpret_cast<__half*>(Y), ldy, partial, sem,
-                             splits, (flags & TL_FLAG_STATIC_WEIGHTS) != 0, bf, s);
+                             splits, (flags & TL_FLAG_STATIC_WEIGHTS) != 0, bf, po, s);
     if (r != TL_ENOFIT) return r;
     // the decode kernel's stage ring does not fit shared memory for this shape: batched path
     path = TL_PATH_TC;
@@ -230,9 +257,45 @@ tl_status tl_matmul_ex(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, 
     return tc_matmul(w, M, N, K, group, reinterpret_cast<const __half*>(A), lda,
                      reinterpret_cast<const uint8_t*>(w_t), reinterpret_cast<const __half*>(scales),
                      reinterpret_cast<const __half*>(zeros), reinterpret_cast<__half*>(Y), ldy, partial, sem,
-                     splits, bf, s);
+                     splits, bf, po, s);
   }
   return fail(TL_EUNSUPPORTED, "unknown path %d", path);
+}
+
+extern "C" {
+
+tl_status tl_matmul_ex(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group, const void* A,
+                       int64_t lda, const void* w_t, const void* scales, const void* zeros, void* Y, int64_t ldy,
+                       void* workspace, size_t workspace_bytes, int32_t path, int32_t splits, uint32_t flags,
+                       void* stream) {
+  return matmul_core(w, a, M, N, K, group, A, lda, w_t, scales, zeros, Y, ldy, workspace, workspace_bytes, path,
+                     splits, flags, nullptr, stream);
+}
+
+tl_status tl_matmul_gathered(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group, const void* A,
+                             int64_t lda, const void* w_t, const void* scales, const void* zeros, void* Y,
+                             int64_t ldy, void* const* Y_peers, uint32_t* const* flag_peers, int32_t npeers,
+                             void* workspace, size_t workspace_bytes, uint32_t flags, void* stream) {
+  if (npeers < 0 || npeers > kMaxPeers) return fail(TL_EINVAL_SHAPE, "npeers=%d outside [0, %d]", npeers, kMaxPeers);
+  if (npeers == 0)
+    return matmul_core(w, a, M, N, K, group, A, lda, w_t, scales, zeros, Y, ldy, workspace, workspace_bytes,
+                       TL_PATH_AUTO, 0, flags, nullptr, stream);
+  if (!Y_peers || !flag_peers) return fail(TL_ENULL, "tl_matmul_gathered: NULL peer arrays");
+  PeerOut po{};
+  for (int i = 0; i < npeers; ++i) {
+    if (!Y_peers[i] || !flag_peers[i]) return fail(TL_ENULL, "tl_matmul_gathered: NULL peer pointer %d", i);
+    if (!aligned16(Y_peers[i]) || (reinterpret_cast<uintptr_t>(flag_peers[i]) & 3u))
+      return fail(TL_EALIGN, "peer %d: Y must be 16-byte and the flag 4-byte aligned", i);
+    po.y[i] = reinterpret_cast<unsigned short*>(Y_peers[i]);
+    po.flag[i] = flag_peers[i];
+  }
+  po.n = npeers;
+  po.signal = 1;
+  if (M == 0) return TL_OK;  // nothing to send: callers do not wait for an empty call
+  if (workspace && workspace_bytes >= kSemBytes && aligned16(workspace))
+    po.done = reinterpret_cast<uint32_t*>(workspace) + kSemBytes / 4 - 1;  // last semaphore word
+  return matmul_core(w, a, M, N, K, group, A, lda, w_t, scales, zeros, Y, ldy, workspace, workspace_bytes,
+                     TL_PATH_AUTO, 0, flags, &po, stream);
 }
 
 tl_status tl_matmul(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group, const void* A,
@@ -247,10 +310,12 @@ tl_status tl_matmul_hostio(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t
                            void* Y_dev, void* Y_host, void* workspace, size_t workspace_bytes, uint32_t flags,
                            void* stream) {
   if (M == 0) return TL_OK;
-  if (a != TL_ACT_F16 && a != TL_ACT_BF16) return fail(TL_EUNSUPPORTED, "unknown activation type %d", (int)a);
+  if (a != TL_ACT_F16 && a != TL_ACT_BF16 && a != TL_ACT_I8)
+    return fail(TL_EUNSUPPORTED, "unknown activation type %d", (int)a);
   if (!A_host || !A_dev || !Y_dev || !Y_host) return fail(TL_ENULL, "tl_matmul_hostio: NULL pointer");
   cudaStream_t s = as_stream(stream);
-  if (cudaMemcpyAsync(A_dev, A_host, (size_t)(M * K * 2), cudaMemcpyHostToDevice, s) != cudaSuccess)
+  const size_t a_bytes = (size_t)(M * K) * (a == TL_ACT_I8 ? 1 : 2);
+  if (cudaMemcpyAsync(A_dev, A_host, a_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess)
     return fail(TL_ECUDA, "H2D copy of A failed");
   tl_status st = tl_matmul_ex(w, a, M, N, K, group, A_dev, K, w_t, scales, zeros, Y_dev, N, workspace,
                               workspace_bytes, TL_PATH_AUTO, 0, flags, stream);

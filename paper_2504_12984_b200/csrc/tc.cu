@@ -32,7 +32,8 @@ static int env_dbg(const char* name) {
 // decode tensor-core path (tcd.cuh): the weight tile and its scale / zero slices ride in one TMA stage
 tl_status tcd_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, const __half* A, int64_t lda,
                      const uint8_t* wt, const __half* scales, const __half* zeros, __half* Y, int64_t ldy,
-                     float* partial, int* sem, int grid_req, bool static_weights, bool bf, cudaStream_t st) {
+                     float* partial, int* sem, int grid_req, bool static_weights, bool bf, const PeerOut* po,
+                     cudaStream_t st) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -55,6 +56,7 @@ tl_status tcd_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, con
   p.dbg = env_dbg("TL_TCD_DBG");
   p.static_w = static_weights ? 1 : 0;
   p.bf = bf ? 1 : 0;
+  if (po) p.po = *po;
   p.magic = 0x64006400u;
   if (getenv("TL_TRACE")) {
     static int launches = 0;  // two trace buffers, alternating per launch (back-to-back overlap)
@@ -183,7 +185,7 @@ tl_status make_tmap_side(CUtensorMap* m, const __half* X, int64_t N, int64_t K, 
 
 tl_status tc_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, const __half* A, int64_t lda,
                     const uint8_t* wt, const __half* scales, const __half* zeros, __half* Y, int64_t ldy,
-                    float* partial, int* sem, int grid_req, bool bf, cudaStream_t st) {
+                    float* partial, int* sem, int grid_req, bool bf, const PeerOut* po, cudaStream_t st) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -208,6 +210,11 @@ tl_status tc_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, cons
     p.magic = 0x64006400u;
     p.dbg = env_dbg("TL_TC2_DBG");
     p.bf = bf ? 1 : 0;
+    if (po) {
+      p.po = *po;
+      for (int i = 0; i < po->n; ++i) p.po.y[i] = po->y[i] + m0 * ldy;
+      p.po.signal = (m0 + 128 >= M) ? 1 : 0;  // the last chunk's launch signals the whole call
+    }
     // stage: [activation boxes NB x 256 B (1024-aligned, 128B swizzle) | weight tile 2p | weight tile 2p+1]
     const uint32_t wb = (uint32_t)tile_bytes(w.bits);
     p.w_off_in_stage = (uint32_t)p.NB * 256;

@@ -47,6 +47,7 @@ struct Tc2Params {
   int* sem;        // [n-pairs]
   uint32_t magic;  // 0x64006400 (a kernel argument: the LOP3 takes one immediate, see tcd)
   int bf;          // 1: bf16 activations / scales / zeros / Y
+  PeerOut po;      // row f3: gathered output fused into the epilogue (peer.cuh); po.n == 0: local only
   int dbg;         // TL_TC2_DBG timing experiments (results invalid): 1 skip partial stores, 2 skip reduction
 };
 
@@ -376,8 +377,13 @@ __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_consta
             const int m = cb + j;
             if (m < p.M) {
               const float v = __uint_as_float(r[j]);
-              if (complete) reinterpret_cast<unsigned short*>(p.Y)[(int64_t)m * p.ldy + col] = Act<BF>::from_float(v);
-              else if (!(p.dbg & 1)) __stcg(part + (int64_t)m * kBN + n, v);
+              if (complete) {
+                const unsigned short h = Act<BF>::from_float(v);
+                reinterpret_cast<unsigned short*>(p.Y)[(int64_t)m * p.ldy + col] = h;
+                peer_store(p.po, (int64_t)m * p.ldy + col, h);
+              } else if (!(p.dbg & 1)) {
+                __stcg(part + (int64_t)m * kBN + n, v);
+              }
             }
           }
         }
@@ -446,7 +452,9 @@ __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_consta
                   const uint2 o = make_uint2(
                       (uint32_t)Act<BF>::from_float(acc[j].x) | ((uint32_t)Act<BF>::from_float(acc[j].y) << 16),
                       (uint32_t)Act<BF>::from_float(acc[j].z) | ((uint32_t)Act<BF>::from_float(acc[j].w) << 16));
-                  *reinterpret_cast<uint2*>(p.Y + (int64_t)m * p.ldy + (2 * np + tj) * kBN + 4 * c4) = o;
+                  const int64_t off = (int64_t)m * p.ldy + (2 * np + tj) * kBN + 4 * c4;
+                  *reinterpret_cast<uint2*>(p.Y + off) = o;
+                  peer_store4(p.po, off, o);
                 }
               }
             }
@@ -462,6 +470,7 @@ __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_consta
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, 512);
+  if (threadIdx.x == 0) peer_signal(p.po, gridDim.x);  // row f3: after every Y store of the CTA
 }
 
 template <class F>

@@ -62,6 +62,7 @@ struct TcdParams {
   uint32_t magic;  // 0x64006400, a kernel argument so that AND-mask + OR-magic fuse into ONE LOP3
                    // (LOP3 takes one immediate; the magic must live in a register)
   int static_w;  // TL_FLAG_STATIC_WEIGHTS: the weight stream may start before griddepcontrol.wait
+  PeerOut po;  // row f3: gathered output fused into the epilogue (peer.cuh); po.n == 0: local only
   int dbg;  // experiment knobs (TL_TCD_DBG; device-side ones only with -DTCD_TRACE): 1 skip MMAs,
             // 4 skip unpack/STTM, 8 skip scale/zero copies, 128 no PDL (host)
 };
@@ -614,8 +615,13 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
         float v = 0.f;
 #pragma unroll
         for (int gg = 0; gg < NG; ++gg) v += red[(gg * p.M + m) * kBN + n];
-        if (complete) reinterpret_cast<unsigned short*>(p.Y)[(int64_t)m * p.ldy + col] = Act<BF>::from_float(v);
-        else __stcg(part + (int64_t)m * kBN + n, v);
+        if (complete) {
+          const unsigned short h = Act<BF>::from_float(v);
+          reinterpret_cast<unsigned short*>(p.Y)[(int64_t)m * p.ldy + col] = h;
+          peer_store(p.po, (int64_t)m * p.ldy + col, h);
+        } else {
+          __stcg(part + (int64_t)m * kBN + n, v);
+        }
       }
       if (!complete) {
         // publish: the CTA barrier orders every thread's partial store before thread 128's
@@ -637,7 +643,9 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
           const int lo = flag[1], hi = flag[2];
           for (int m = g; m < p.M; m += NG) {
             const float sum = streamk_sum(p.partial, lo, hi, flag[3], (int64_t)kTcdNB * kBN, (int64_t)m * kBN + n);
-            reinterpret_cast<unsigned short*>(p.Y)[(int64_t)m * p.ldy + col] = Act<BF>::from_float(sum);
+            const unsigned short h = Act<BF>::from_float(sum);
+            reinterpret_cast<unsigned short*>(p.Y)[(int64_t)m * p.ldy + col] = h;
+            peer_store(p.po, (int64_t)m * p.ldy + col, h);
           }
           if (threadIdx.x == 128) p.sem[nt] = 0;
         }
@@ -652,6 +660,7 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, 512);
+  if (threadIdx.x == 0) peer_signal(p.po, gridDim.x);  // row f3: after every Y store of the CTA
   if (threadIdx.x == 0) tcd_stamp(p, 7);
 }
 

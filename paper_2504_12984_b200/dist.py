@@ -5,8 +5,12 @@ independent output tiles), so a column shard needs no communic
 to compute.  Rank r owns columns [n0, n1) = column_shard(N, world, r): contiguous,
 multiples of 128 (the transformed layout's tile width).  Each rank transforms its own
 shard once (tl_transform_weights) and runs tl_matmul on it; only the *gathered* variant
-exchanges data: one all-gather of the Y shards (NCCL over NVLink on B200; any
-torch.distributed backend works, the CPU tests use gloo).
+exchanges data: either one all-gather of the Y shards after the matmul (NCCL over NVLink on B200;
+any torch.distributed backend works, the CPU tests use gloo), or -- row f3 -- no collective at all:
+``FusedGather`` maps every rank's gathered buffer into every other rank (CUDA IPC handles,
+exchanged once over the process group) and the matmul kernel's epilogue stores each finished
+element straight into all of them over NVLink (``tl_matmul_gathered``), then signals per-rank
+flags that the consumer waits on (``tl_gather_wait``).
 
 This module holds shard arithmetic and the collective only; every matmul runs in the
 CUDA library through ``_lib``.
@@ -49,6 +53,64 @@ def gather_columns(Y_shard: torch.Tensor, N: int, world: int, group=None) -> tor
     if M == 1:
         return buf.view(1, N)            # rank-major columns are already contiguous
     return buf.permute(1, 0, 2).reshape(M, N)
+
+
+def peer_pointers(y_bases: list[int], flag_bases: list[int], rank: int, n0: int,
+                  elem_bytes: int = 2) -> tuple[list[int], list[int]]:
+    """Addresses rank `rank` passes to tl_matmul_gathered (row f3): for every OTHER rank q, the
+    address of column n0 of q's gathered buffer (row 0; the row stride is the full N) and of q's
+    flag slot `rank`.  `y_bases` / `flag_bases` are the ranks' buffer base addresses as mapped in
+    this process."""
+    if len(y_bases) != len(flag_bases) or not 0 <= rank < len(y_bases):
+        raise ValueError("one gathered buffer and one flag array per rank")
+    ys = [b + n0 * elem_bytes for q, b in enumerate(y_bases) if q != rank]
+    fs = [f + 4 * rank for q, f in enumerate(flag_bases) if q != rank]
+    return ys, fs
+
+
+def exchange(obj, world: int, group=None) -> list:
+    """All ranks' `obj` (picklable), rank order (one torch.distributed all_gather_object)."""
+    out = [None] * world
+    dist.all_gather_object(out, obj, group=group)
+    return out
+
+
+class FusedGather:
+    """Row f3: gathered outputs of an [M, N] column-sharded layer with the all-gather fused into the
+    matmul epilogue.  Holds `nbuf` gathered buffers [M, N] and one flag array [world] per rank,
+    mapped into every rank through CUDA IPC handles exchanged once over `group`.  Successive calls
+    alternate the buffers (the ordering contract of tl_matmul_gathered)."""
+
+    def __init__(self, M: int, N: int, world: int, rank: int, group=None, nbuf: int = 2,
+                 dtype=torch.float16):
+        from torch.multiprocessing.reductions import reduce_tensor
+        self.M, self.N, self.world, self.rank, self.nbuf = M, N, world, rank, nbuf
+        self.Yg = [torch.empty((M, N), dtype=dtype, device="cuda") for _ in range(nbuf)]
+        self.flags = torch.zeros(world, dtype=torch.int32, device="cuda")
+        torch.cuda.synchronize()
+        mine = [reduce_tensor(t) for t in self.Yg + [self.flags]]
+        self._peer_tensors = []     # keeps the IPC mappings alive
+        y_bases = [[0] * world for _ in range(nbuf)]
+        f_bases = [0] * world
+        for q, payload in enumerate(exchange(mine, world, group)):
+            ts = self.Yg + [self.flags] if q == rank else [fn(*args) for fn, args in payload]
+            self._peer_tensors.append(ts)
+            for b in range(nbuf):
+                y_bases[b][q] = ts[b].data_ptr()
+            f_bases[q] = ts[nbuf].data_ptr()
+        self.y_bases, self.f_bases = y_bases, f_bases
+        self.epoch = 0
+
+    def __call__(self, layer: "ShardedA16WxLinear", A: torch.Tensor) -> torch.Tensor:
+        """Y = the gathered [M, N] output of `layer` (this rank's shard) for activations A."""
+        self.epoch += 1
+        b = self.epoch % self.nbuf
+        ys, fs = peer_pointers(self.y_bases[b], self.f_bases, self.rank, layer.n0)
+        Y = self.Yg[b]
+        L.tl_matmul_gathered(layer.w, A.shape[0], layer.Ns, layer.K, layer.G, A, layer.w_t, layer.scales,
+                             layer.zeros, Y[:, layer.n0:], self.N, ys, fs, layer._workspace(A.shape[0]))
+        L.tl_gather_wait(self.flags, self.world, self.rank, self.epoch)
+        return Y
 
 
 class ShardedA16WxLinear:

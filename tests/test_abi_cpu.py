@@ -86,6 +86,19 @@ def test_bad_arguments_rejected_before_any_launch(lib):
     assert lib._lib._tl_status_str(st).decode() == "TL_EUNSUPPORTED"
     assert lib.tl_matmul_workspace_bytes(w, 1, 128, 128, 128, atype=7) == 0
     assert lib.tl_matmul_workspace_bytes(w, 1, 128, 128, 128, atype=lib.TL_ACT_BF16) > 0
+    # int8 activations (row f4): the workspace grows by the staged fp16 copy of A (2*M*K bytes, 256-aligned)
+    f16 = lib.tl_matmul_workspace_bytes(w, 3, 256, 512, 128)
+    assert lib.tl_matmul_workspace_bytes(w, 3, 256, 512, 128, atype=lib.TL_ACT_I8) == (f16 + 255) // 256 * 256 + 2 * 3 * 512
+    # int8 rows need 16-byte strides in BYTES: lda = 8 int8 elements is misaligned, 16 is fine (then NULL ws)
+    st = lib._lib._tl_matmul(w, lib.TL_ACT_I8, 1, 128, 128, 128, 16, 136, 16, 16, None, 16, 128, 16, 1 << 24, None)
+    assert lib._lib._tl_status_str(st).decode() == "TL_EALIGN"
+    st = lib._lib._tl_matmul(w, lib.TL_ACT_I8, 1, 128, 128, 128, 16, 144, 16, 16, None, 16, 128, 0, 1 << 24, None)
+    assert lib._lib._tl_status_str(st).decode() == "TL_EWORKSPACE"
+    # MX scale conversion: argument checks only (no launch on CPU)
+    assert lib._lib._tl_status_str(lib._lib._tl_mx_scales_to_f16(16, -1, 0, 16, None)).decode() == "TL_EINVAL_SHAPE"
+    assert lib._lib._tl_status_str(lib._lib._tl_mx_scales_to_f16(None, 4, 0, 16, None)).decode() == "TL_ENULL"
+    assert lib._lib._tl_status_str(lib._lib._tl_mx_scales_to_f16(16, 4, 65, 16, None)).decode() == "TL_EINVAL_SHAPE"
+    assert lib._lib._tl_mx_scales_to_f16(16, 0, 0, 16, None) == 0
     # tl_matmul_ex: unknown flags / paths, negative splits
     def ex(path=0, splits=0, flags=0):
         return lib._lib._tl_status_str(lib._lib._tl_matmul_ex(w, 0, 1, 128, 128, 128, 16, 128, 16, 16, None, 16,

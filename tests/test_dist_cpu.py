@@ -95,3 +95,51 @@ def test_bench_relaunches_itself_with_one_process_per_gpu():
     assert argv[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
     assert "--nproc-per-node=4" in argv and "--master-addr=127.0.0.1" in argv and "--master-port=29555" in argv
     assert argv[-4:] == ["--gpus", "4", "--steps", "7"] and argv[-5].endswith("bench.py")
+
+
+def _fused_worker(rank, world, port, M, N, out_dir):
+    """Row f3 host logic: exchange fake buffer bases, derive the peer addresses with peer_pointers,
+    and 'store' this rank's shard into every rank's buffer at those addresses (a byte-addressed
+    numpy arena stands in for the mapped device memory).  Every rank's buffer must end up equal to
+    the full Y, and every flag slot must be hit once by its owner rank."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2504_12984_b200.dist import column_shard, exchange, peer_pointers
+    ybytes = M * N * 2
+    y_base = (1 << 24) * (rank + 1)                               # disjoint fake address ranges
+    f_base = (1 << 30) + 64 * rank
+    bases = exchange((y_base, f_base), world)
+    y_bases = [b[0] for b in bases]
+    f_bases = [b[1] for b in bases]
+    assert y_bases[rank] == y_base and len(set(y_bases)) == world
+    n0, n1 = column_shard(N, world, rank)
+    ys, fs = peer_pointers(y_bases, f_bases, rank, n0)
+    assert len(ys) == world - 1
+    Yfull = (np.arange(M * N, dtype=np.float64).reshape(M, N) % 2039).astype(np.float16)
+    writes = []
+    for q_addr, f_addr in zip(ys, fs):
+        q = [i for i, b in enumerate(y_bases) if b <= q_addr < b + ybytes][0]
+        assert f_bases[q] + 4 * rank == f_addr
+        col0 = (q_addr - y_bases[q]) // 2
+        assert col0 == n0
+        writes.append((q, col0))
+    allw = exchange(writes, world)
+    if rank == 0:
+        bufs = [np.full((M, N), np.nan, np.float16) for _ in range(world)]
+        for r, ws_ in enumerate(allw):
+            a, b = column_shard(N, world, r)
+            bufs[r][:, a:b] = Yfull[:, a:b]                       # the rank's local store
+            for q, c0 in ws_:
+                bufs[q][:, c0:c0 + (b - a)] = Yfull[:, a:b]       # the replicated epilogue stores
+        for q in range(world):
+            assert np.array_equal(bufs[q].view(np.uint16), Yfull.view(np.uint16)), q
+        np.save(os.path.join(out_dir, "ok.npy"), np.ones(1))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fused_gather_peer_addresses(tmp_path, world):
+    mp.spawn(_fused_worker, args=(world, _free_port(), 3, 1024, str(tmp_path)), nprocs=world, join=True)
+    assert (tmp_path / "ok.npy").exists()

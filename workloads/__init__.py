@@ -105,6 +105,19 @@ def gen_activations(M: int, K: int, seed: int) -> np.ndarray:
     return rng.standard_normal(size=(M, K)).astype(np.float16)
 
 
+def gen_activations_i8(M: int, K: int, seed: int) -> np.ndarray:
+    """A [M, K] int8, uniform over all 256 values (row f4: int8 activations)."""
+    rng = np.random.Generator(np.random.PCG64(seed + 6))
+    return rng.integers(-128, 128, size=(M, K), dtype=np.int8)
+
+
+def gen_mx_exponents(K: int, N: int, seed: int, center: int, spread: int = 3) -> np.ndarray:
+    """E8M0 block-scale codes [K/32, N] uint8, uniform in [center - spread, center + spread]
+    (row f4: microscaling, one code per block of 32 weights along K)."""
+    rng = np.random.Generator(np.random.PCG64(seed + 7))
+    return rng.integers(center - spread, center + spread + 1, size=(K // 32, N)).astype(np.uint8)
+
+
 def gen_exact_instance(fmt: str, M: int, K: int, N: int, group: int, seed: int, j: int = 0):
     """Exact-integer instance: A in {-1,0,1}, s = 2^-j, integer zeros.
 
