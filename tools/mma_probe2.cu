@@ -3,6 +3,7 @@
 // its own accumulators).  Reports the SM-wide cycles per MMA: if two issuers halve it, the
 // single-thread floor is an issue-side latency, not tensor-pipe occupancy.
 #include <cstdio>
+#include <cstdlib>
 
 #include "ptx.cuh"
 
@@ -18,7 +19,10 @@ __device__ __forceinline__ uint64_t sw128(uint32_t saddr) {
   return d;
 }
 
-__global__ void mma_kernel(int M, int N, int reps, int ncols, int issuers, int ts, long long* out) {
+// kind: 0 = kind::f16 (K = 16), 1 = kind::i8 (K = 32); fresh: the TS A operand cycles over 32
+// different 8-column TMEM chunks (as the decode kernel's W^T slots), else one fixed chunk
+__global__ void mma_kernel(int M, int N, int reps, int ncols, int issuers, int ts, long long* out, int kind = 0,
+                           int fresh = 0) {
   extern __shared__ __align__(1024) uint8_t sm[];  // A: 128 rows x 128 B, B: 256 rows x 128 B
   __shared__ uint64_t bar[2];
   __shared__ uint32_t slot;
@@ -40,7 +44,8 @@ __global__ void mma_kernel(int M, int N, int reps, int ncols, int issuers, int t
   const uint32_t tmem = slot;
   long long t0 = clock64();
   if (warp < issuers) {
-    const uint32_t idesc = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+    const uint32_t idesc = kind ? ((2u << 4) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24))
+                                : ((1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24));
     const uint32_t abase = smem_u32(sm), bbase = smem_u32(sm + 16384);
     // accumulator region of this issuer: N columns; A (TS) operand: 8 columns after all accumulators
     const uint32_t acc = tmem + warp * N;
@@ -50,11 +55,16 @@ __global__ void mma_kernel(int M, int N, int reps, int ncols, int issuers, int t
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const uint64_t bd = sw128(bbase + j * 32);
-          if (ts) {
+          if (ts && kind) {
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(acc),
+                "r"(fresh ? tmem + 256 + ((r + j) & 31) * 8 : aop), "l"(bd), "r"(idesc), "r"(1u));
+          } else if (ts) {
             asm volatile(
                 "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                 "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(acc),
-                "r"(aop), "l"(bd), "r"(idesc), "r"(1u));
+                "r"(fresh ? tmem + 256 + ((r + j) & 31) * 8 : aop), "l"(bd), "r"(idesc), "r"(1u));
           } else {
             const uint64_t ad = sw128(abase + j * 32);
             asm volatile(
@@ -81,6 +91,23 @@ int main() {
   cudaMalloc(&d, 8 * 4096);
   const int smem = 49152 + 1024;
   cudaFuncSetAttribute(mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  // fresh-A TS operands (the decode kernel's case): kind::f16 vs kind::i8, one issuer, 1 CTA/SM
+  for (int kind = 0; kind < 2; ++kind)
+    for (int fresh = 0; fresh < 2; ++fresh)
+      for (int N : {16, 32, 64, 128}) {
+        const int reps = 2048;
+        mma_kernel<<<148, 128, smem>>>(128, N, reps, 512, 1, 1, d, kind, fresh);
+        cudaError_t e = cudaDeviceSynchronize();
+        long long h[148];
+        cudaMemcpy(h, d, 8 * 148, cudaMemcpyDeviceToHost);
+        long long mx = 0;
+        for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
+        printf("TS %s M=128 N=%3d A=%s: %.1f cycles per MMA (%.1f weights/clk)  %s\n", kind ? "i8 " : "f16", N,
+               fresh ? "fresh" : "fixed", (double)mx / reps, (kind ? 4096.0 : 2048.0) * reps / mx,
+               e == cudaSuccess ? "ok" : cudaGetErrorString(e));
+        if (e != cudaSuccess) return 1;
+      }
+  if (getenv("PROBE_ALL") == nullptr) return 0;
   for (int ts = 1; ts >= 0; --ts)
     for (int M : {128, 64})
       for (int N : {16, 32, 64, 128, 256})
