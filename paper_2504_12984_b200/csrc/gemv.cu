@@ -21,6 +21,10 @@ tl_status gemv_dispatch(tl_wtype w, const GemvParams& p, int grid_req, cudaStrea
 
 template <class F>
 tl_status launch_gv1(const Gv1Params& p, const CUtensorMap* tmap, int grid, uint32_t smem_bytes, cudaStream_t st);
+#define TL_EXTERN_GV1(K, B, E)                                                                                 \
+  extern template tl_status launch_gv1<Fmt<K, B, E>>(const Gv1Params&, const CUtensorMap*, int, uint32_t, cudaStream_t);
+TL_FOR_EACH_FORMAT(TL_EXTERN_GV1)
+#undef TL_EXTERN_GV1
 tl_status make_tmap_side(CUtensorMap* m, const __half* X, int64_t N, int64_t K, int32_t G, int R);
 
 bool gv1_eligible(int64_t M, int64_t K, int32_t G) { return M == 1 && G % kBK == 0 && K * 2 <= 65536; }

@@ -14,6 +14,11 @@ namespace tl {
 template <class F>
 tl_status launch_dq16(const uint8_t* wt, const __half* scales, const __half* zeros, __half* out, int N, int K, int G,
                       int nt0, int ntiles, bool bf, cudaStream_t st);
+#define TL_EXTERN_DQ16(K, B, E)                                                                            \
+  extern template tl_status launch_dq16<Fmt<K, B, E>>(const uint8_t*, const __half*, const __half*, __half*, int, \
+                                                      int, int, int, int, bool, cudaStream_t);
+TL_FOR_EACH_FORMAT(TL_EXTERN_DQ16)
+#undef TL_EXTERN_DQ16
 
 constexpr size_t kCublasWs = 32u << 20;     // cuBLAS workspace (set explicitly: no allocation, graph-capturable)
 constexpr size_t kChunkBytes = 64u << 20;   // decoded W^T chunk (stays in the 126 MB L2 for the GEMM)

@@ -18,6 +18,16 @@ tl_status launch_tc2(const Tc2Params& p, const CUtensorMap* tmap, int grid, uint
 template <class F>
 tl_status launch_tcd(const TcdParams& p, const CUtensorMap* tmap, int grid, uint32_t smem_bytes, cudaStream_t st);
 
+// the kernels are instantiated one format per generated translation unit (build.py): keep this
+// one from instantiating all 37 formats' kernels again
+#define TL_EXTERN_TC(K, B, E)                                                                              \
+  extern template tl_status launch_tc2<Fmt<K, B, E>>(const Tc2Params&, const CUtensorMap*, int, uint32_t,   \
+                                                     cudaStream_t);                                       \
+  extern template tl_status launch_tcd<Fmt<K, B, E>>(const TcdParams&, const CUtensorMap*, int, uint32_t,   \
+                                                     cudaStream_t);
+TL_FOR_EACH_FORMAT(TL_EXTERN_TC)
+#undef TL_EXTERN_TC
+
 static tl_status make_tmap_a(CUtensorMap* m, const __half* A, int64_t M, int64_t K, int64_t lda, int NB);
 
 long long* g_trace = nullptr;  // debug: clock64 stamps of CTA 0 (TL_TRACE=1)
@@ -75,8 +85,7 @@ tl_status tcd_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, con
   const uint32_t red = (uint32_t)kTcdNG * (uint32_t)M * kBN * 4;
   const uint32_t opb = kTcdMaxNOP * kTcdOpBytes;
   const uint32_t stash = p.rot ? (uint32_t)(K * 2) : 0u;
-  const uint64_t fixed = 1024 /*align*/ + (uint64_t)opb + stash + red + 2048 /*barriers, tmem slot, flags*/ +
-                         2048 /*raw-int decode: per-k-tile activation meta, K/128 <= 256 entries*/;
+  const uint64_t fixed = 1024 /*align*/ + (uint64_t)opb + stash + red + 2048 /*barriers, tmem slot, flags*/;
   if (fixed + 3ull * p.stage_bytes > 227u * 1024u)
     return TL_ENOFIT;  // caller falls back to the batched path
   int ns = (int)((227u * 1024u - fixed) / p.stage_bytes);
@@ -87,8 +96,8 @@ tl_status tcd_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, con
   p.stash_off = p.op_off + opb;
   p.red_off = p.stash_off + ((stash + 127) & ~127u);
   p.bar_off = (p.red_off + red + 15) & ~15u;
-  p.meta_off = (p.bar_off + (2 * ns + 2 * kTcdMaxNOP + 2 * kTcdMaxNW + 2 * kTcdMaxNACC + 1) * 8 + 32 + 15) & ~15u;
-  const uint32_t smem = p.meta_off + 2048 + 1024;
+  const uint32_t smem =
+      p.bar_off + (2 * ns + 2 * kTcdMaxNOP + 2 * kTcdMaxNW + 2 * kTcdMaxNACC + 1) * 8 + 32 + 1024;
   if (smem > 227 * 1024) return TL_ENOFIT;
   CUtensorMap tmap;
   tl_status s = make_tmap_a(&tmap, A, M, K, lda, kTcdNB);

@@ -62,7 +62,6 @@ struct TcdParams {
   uint32_t magic;  // 0x64006400, a kernel argument so that AND-mask + OR-magic fuse into ONE LOP3
                    // (LOP3 takes one immediate; the magic must live in a register)
   int static_w;  // TL_FLAG_STATIC_WEIGHTS: the weight stream may start before griddepcontrol.wait
-  uint32_t meta_off;  // raw-int decode: per-k-tile (2^(24 - sigma - Pmax), sum a) [K/128] (float2)
   PeerOut po;  // row f3: gathered output fused into the epilogue (peer.cuh); po.n == 0: local only
   int dbg;  // experiment knobs (TL_TCD_DBG; device-side ones only with -DTCD_TRACE): 1 skip MMAs,
             // 4 skip unpack/STTM, 8 skip scale/zero copies, 128 no PDL (host)
@@ -161,26 +160,6 @@ __host__ __device__ constexpr bool plan_uses_p(int P) {
   return false;
 }
 
-// the largest field position P of an int format's plan, and the plan's P of pair i (0..31) packed
-// as 4-bit nibbles (runtime lookup without a local-memory table)
-template <class F>
-__host__ __device__ constexpr int plan_pmax() {
-  int m = 0;
-  for (int i = 0; i < 32; ++i) m = kPlan<F::kind, F::bits, F::exp>.pr[i].P > m ? kPlan<F::kind, F::bits, F::exp>.pr[i].P : m;
-  return m;
-}
-template <class F>
-__host__ __device__ constexpr uint64_t plan_p_nibbles(int half) {
-  uint64_t v = 0;
-  for (int i = 0; i < 16; ++i) v |= (uint64_t)kPlan<F::kind, F::bits, F::exp>.pr[16 * half + i].P << (4 * i);
-  return v;
-}
-template <class F>
-__device__ __forceinline__ int plan_p(int i) {  // i in 0..31
-  constexpr uint64_t lo = plan_p_nibbles<F>(0), hi = plan_p_nibbles<F>(1);
-  return (int)(((i < 16 ? lo : hi) >> (4 * (i & 15))) & 15u);
-}
-
 // Pipeline tracing (tools/trace_tcd.py, tools/trace_pdl.py): compiled in only with -DTCD_TRACE,
 // so the production kernel carries no trace branches.
 #ifdef TCD_TRACE
@@ -214,14 +193,6 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr bool kInt = F::kind != kFloat;  // integer codes: magic form + HFMA2 (u - z)
-  // Decode (M = 1) with fp16 activations, int / uint weights: "raw" codes.  The field of pair i sits
-  // at bits [P_i, P_i + b) of each half with every other bit zero: an exact fp16 SUBNORMAL
-  // u * 2^(P_i - 24), so the unpack is ONE LOP3 per pair (no magic, no HFMA2).  The activation row
-  // carries the rest: a'_k = a_k * 2^(sigma + Pmax - P(k)) (exact power-of-two scaling, sigma per
-  // k-tile so max |a'| lies in [2^14, 2^15)), making every product a_k u_k 2^(sigma + Pmax - 24);
-  // the fixup takes Y += s * (2^(24 - sigma - Pmax) D - z * sum_k a_k) in fp32 (z: the zero point,
-  // 2^(b-1) for the offset-binary ints).  No large offset enters the MMA's fp32 sum.
-  constexpr bool kRaw = kInt && MT == 1 && !BF;
   constexpr uint32_t WB = tile_bytes(F::bits);
   constexpr int kR = tcd_tiles_per_stage(F::bits);
   using Cfg = TcdCfg<MT>;
@@ -312,45 +283,6 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
     if (threadIdx.x == 64) tcd_stamp(p, 11);
   }
 
-  if constexpr (kRaw) {
-    // ---- raw-int prologue (warps 2, 4..19): A[0, :] into the stash, then every k-tile's 128 values
-    // rescaled in place to a'_k = a_k 2^(sigma + Pmax - P(k)) (fp16, exact) with meta[kt] =
-    // (2^(24 - sigma - Pmax), sum_k a_k).  Lane l owns k = 4l .. 4l+3 = pairs 2l, 2l+1 of the tile.
-    if (warp == 2 || warp >= 4) {
-      if (warp == 2 && lane == 0) {  // after griddepcontrol.wait: A is the previous grid's output
-        mbar_arrive_expect_tx(stash_bar, (uint32_t)p.K * 2u);
-        tma_bulk_g2s(smem + p.stash_off, p.A, (uint32_t)p.K * 2u, stash_bar, policy_evict_last());
-      }
-      constexpr int PM = plan_pmax<F>();
-      const int p0 = plan_p<F>((2 * lane) & 31), p1 = plan_p<F>((2 * lane + 1) & 31);
-      mbar_wait(stash_bar, 0);
-      uint8_t* stash = smem + p.stash_off;
-      float2* meta = reinterpret_cast<float2*>(smem + p.meta_off);
-      for (int kt = (warp == 2 ? 0 : warp - 3); kt < KT; kt += 17) {
-        uint2* src = reinterpret_cast<uint2*>(stash + kt * 256 + lane * 8);
-        const uint2 v = *src;
-        const float2 f01 = __half22float2(*reinterpret_cast<const __half2*>(&v.x));
-        const float2 f23 = __half22float2(*reinterpret_cast<const __half2*>(&v.y));
-        float mx = fmaxf(fmaxf(fabsf(f01.x), fabsf(f01.y)), fmaxf(fabsf(f23.x), fabsf(f23.y)));
-        float sa = (f01.x + f01.y) + (f23.x + f23.y);
-#pragma unroll
-        for (int d = 16; d >= 1; d >>= 1) {
-          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, d));
-          sa += __shfl_xor_sync(0xffffffffu, sa, d);
-        }
-        const int e = mx > 0.f ? (int)((__float_as_uint(mx) >> 23) & 0xFF) - 127 : 0;  // floor(log2 max)
-        const int sg = 14 - e - PM;                                                     // sigma
-        const float u0s = __uint_as_float((uint32_t)(127 + sg + PM - p0) << 23);       // exact powers of 2
-        const float u1s = __uint_as_float((uint32_t)(127 + sg + PM - p1) << 23);
-        const __half2 o01 = __floats2half2_rn(f01.x * u0s, f01.y * u0s);
-        const __half2 o23 = __floats2half2_rn(f23.x * u1s, f23.y * u1s);
-        *src = make_uint2(*reinterpret_cast<const uint32_t*>(&o01), *reinterpret_cast<const uint32_t*>(&o23));
-        if (lane == 0) meta[kt] = make_float2(__uint_as_float((uint32_t)(127 + 24 - sg - PM) << 23), sa);
-      }
-      named_bar_sync(3, 17 * 32);
-    }
-  }
-
   if (warp == 0 || warp == 2) {
     // ------------------------------ TMA producers ------------------------------
     // warp 0: the stage = packed weight tile + its scale / zero-point row slices (HBM streams,
@@ -409,7 +341,7 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
         // o = t % 8 gets A[0, kt*128 .. +128) in row r = t % 16 (128B-swizzled K-major: two 64-k
         // blocks of 16 rows x 128 B; 16-byte chunk c of row r at chunk c ^ (r % 8)) and the row it
         // held for tile t - 8, (r + 8) % 16, zeroed.  Lane l moves k = 4l .. 4l+3.
-        if (!kRaw && lane == 0) {  // after griddepcontrol.wait: A is the previous grid's output (raw: prologue)
+        if (lane == 0) {  // after griddepcontrol.wait: A is the previous grid's output
           mbar_arrive_expect_tx(stash_bar, (uint32_t)p.K * 2u);
           tma_bulk_g2s(smem + p.stash_off, p.A, (uint32_t)p.K * 2u, stash_bar, policy_evict_last());
         }
@@ -521,21 +453,10 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
 #pragma unroll
     for (int m = 0; m < MT; ++m) tot[m] = 0.f;
 
-    auto fixup = [&](int tp, float c1, float zf) {
+    auto fixup = [&](int tp, float c1) {
       const int a = tp % NACC;
       mbar_wait(&full_acc[a], (uint32_t)(tp / NACC) & 1);
       tc_fence_after();
-      if constexpr (kRaw) {
-        const uint32_t d = tcd_ldtm_x1(tmem + lane_off + kTcdAccCol + ((tp >> 4) & 1) * kTcdNB + (tp & 15));
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        int kt = u0 + tp;  // k-tile of tile tp
-        kt -= (kt / KT) * KT;
-        const float2 mt = reinterpret_cast<const float2*>(smem + p.meta_off)[kt];
-        tot[0] = fmaf(c1, fmaf(mt.x, __uint_as_float(d), -zf * mt.y), tot[0]);
-        return;
-      }
       const uint32_t ta = Cfg::kRot ? tmem + lane_off + kTcdAccCol + ((tp >> 4) & 1) * kTcdNB + (tp & 15)
                                     : tmem + lane_off + kTcdAccCol + a * kTcdNB;
       if constexpr (MT == 1) {
@@ -564,7 +485,6 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
     // reached it by then: tp2 (older) and tp1 are pending, with their scale * c1mul
     int tp1 = -1, tp2 = -1;
     float c1p1 = 0.f, c1p2 = 0.f;
-    float zp1 = 0.f, zp2 = 0.f;  // raw ints: the pending tiles' zero points
     int t0 = 0;
     while (t0 < T) {
       const int ufirst = u0 + t0;
@@ -582,14 +502,7 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
         const float sc = Act<BF>::to_float(lds16(st + kR * WB + 256 * jt + 2 * n));
         // ints: -z as fp16x2 (zero point of the tile's group; offset-binary ints: 2^(b-1))
         uint32_t zneg = 0;
-        float zf = 0.f;  // raw ints: z (uint: the group's zero point, int: 2^(b-1))
-        if constexpr (kRaw) {
-          if constexpr (F::kind == kUint) {
-            if (has_zeros) zf = __half2float(__ushort_as_half(lds16(st + kR * WB + kR * 256 + 256 * jt + 2 * n)));
-          } else {
-            zf = (float)(1 << (F::bits - 1));
-          }
-        } else if constexpr (kInt) {
+        if constexpr (kInt) {
           if constexpr (F::kind == kUint) {
             if (has_zeros) {
               const uint32_t zb = Act<BF>::neg_zero_h(lds16(st + kR * WB + kR * 256 + 256 * jt + 2 * n));
@@ -608,7 +521,7 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
         uint32_t cp[10];
         static_for<0, 10>([&](auto PP) {
           constexpr int P = decltype(PP)::value;
-          if constexpr (kInt && !kRaw && plan_uses_p<F>(P)) {
+          if constexpr (kInt && plan_uses_p<F>(P)) {
             constexpr uint32_t k = 0x8000u | ((uint32_t)(25 - P) << 10);  // fp16 -2^(10-P)
             cp[P] = h2_as_u32(__hadd2(u32_as_h2(zneg), u32_as_h2(k | (k << 16))));
           }
@@ -622,7 +535,7 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
           for (int j = 0; j < 2 * F::bits; ++j) bw[j] = words[tile_word(h, j)];
           static_for<0, 16>([&](auto II) {
             constexpr int i = (c & 1) * 16 + decltype(II)::value;  // pair within the block
-            if constexpr (kInt && !kRaw) {
+            if constexpr (kInt) {
               constexpr int P = kPlan<F::kind, F::bits, F::exp>.pr[i].P;
               const uint32_t x = extract_pair<F, i>(bw, p.magic);
               r[decltype(II)::value] = Act<BF>::from_h2(
@@ -664,17 +577,15 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
           ++lapw;
         }
         if constexpr (Cfg::Lag == 2) {
-          if (tp2 >= 0) fixup(tp2, c1p2, zp2);
+          if (tp2 >= 0) fixup(tp2, c1p2);
           tp2 = tp1;
           c1p2 = c1p1;
-          zp2 = zp1;
         } else {
-          if (tp1 >= 0) fixup(tp1, c1p1, zp1);
+          if (tp1 >= 0) fixup(tp1, c1p1);
         }
         tcd_istamp(p, dw, lane, kk, 6);
         tp1 = t;
         c1p1 = sc * c1mul;
-        zp1 = zf;
         {
           const int qn = (t + NG) / kR;
           s += qn - qst;
@@ -686,8 +597,8 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
         }
       }
       if (dw == 0 && lane == 0) tcd_stamp(p, 5);
-      if (tp2 >= 0) fixup(tp2, c1p2, zp2);
-      if (tp1 >= 0) fixup(tp1, c1p1, zp1);
+      if (tp2 >= 0) fixup(tp2, c1p2);
+      if (tp1 >= 0) fixup(tp1, c1p1);
       tp1 = tp2 = -1;
       if (dw == 0 && lane == 0) tcd_stamp(p, 6);
       // ---- n-tile nt done by this CTA: sum the groups' totals, write Y or a stream-K partial ----

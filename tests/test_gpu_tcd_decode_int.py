@@ -1,7 +1,7 @@
-"""GPU parity of the decode kernel's raw-int scheme (tcd.cuh kRaw: M = 1, int / uint weights, fp16
-activations; reading R27): each code is its exact fp16 subnormal u * 2^(P - 24) (one LOP3 per pair),
-the activation row carries the per-pair 2^-P and a per-k-tile power-of-two range scale, and the
-fixup applies s * (2^(24 - sigma - Pmax) D - z * sum a)."""
+"""GPU parity of the decode kernel (tcd.cuh, M = 1 decode configuration) on every int / uint format:
+three shapes incl. G = 256 and G = K, full-range zero points, activations spanning the whole fp16
+range within one k-tile (an all-zero tile, +-2^-24, 6e4 next to 1e-3), and exact-integer instances
+bit-exact under four stream-K splits."""
 
 import numpy as np
 import pytest
@@ -39,7 +39,7 @@ def test_i8_decode_parity(env, fmt, K, N, G):
 @pytest.mark.parametrize("fmt", ["u4", "u8", "i5", "i8"])
 def test_i8_decode_dynamic_range(env, fmt):
     """Tiles whose activations span the whole fp16 range (one element near 6e4 next to subnormals,
-    an all-zero tile, a tile of +-2^-24): the per-k-tile range scale keeps the error far inside O7."""
+    an all-zero tile, a tile of +-2^-24): the error stays far inside O7."""
     P, torch = env
     K, N, G = 1024, 256, 128
     seed = wl.stable_seed("rawdr", fmt)
@@ -60,9 +60,9 @@ def test_i8_decode_dynamic_range(env, fmt):
 @pytest.mark.parametrize("fmt", ["u1", "u3", "u7", "u8", "i2", "i5", "i8"])
 @pytest.mark.parametrize("splits", [0, 1, 7, 33])
 def test_i8_decode_exact_integer_instance(env, fmt, splits):
-    """A in {-1, 0, 1}, s = 2^-3, K = 4096: the scaled row a' = +-2^(14 - P) and the subnormal codes
-    make every product and partial sum an exact multiple of one power of two, so Y must equal
-    RN_f16(Y64) bit for bit under any stream-K split."""
+    """A in {-1, 0, 1}, s = 2^-3, K = 4096: every per-tile sum is an exact integer and every partial
+    sum an exact multiple of 2^-3 below 2^21, so Y must equal RN_f16(Y64) bit for bit under any
+    stream-K split."""
     P, torch = env
     K, N, G = 4096, 384, 128
     A, codes, s, z = wl.gen_exact_instance(fmt, 1, K, N, G, seed=wl.stable_seed("rawexact", fmt), j=3)

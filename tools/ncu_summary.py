@@ -50,7 +50,28 @@ def source(rep, top=25):
     lines = [f"total executed warp-instructions {tot}"]
     for op, n in c.most_common(top):
         lines.append(f"  {op:10s} {n:11d} {n / tot * 100:5.1f}%  stall samples {st[op]}")
+    # the SASS instructions with the most stall samples (which wait / which dependency)
+    i_addr = h.index("Address") if "Address" in h else None
+    ranked = sorted((r for r in rows if (r[i_st] or "0").isdigit()), key=lambda r: -int(r[i_st] or 0))
+    total_st = sum(int(r[i_st] or 0) for r in rows if (r[i_st] or "0").isdigit()) or 1
+    lines.append(f"top SASS by stall samples (of {total_st})")
+    for r in ranked[:30]:
+        lines.append(f"  {int(r[i_st]):6d} {int(r[i_st]) / total_st * 100:5.1f}%  {r[i_addr] if i_addr is not None else ''}  {r[i_src][:90]}")
     return "\n".join(lines)
+
+
+def stalls(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(io.StringIO(out)))
+    h, vals = r[0], r[2]
+    res = []
+    for i, n in enumerate(h):
+        if "issue_stalled" in n and n.endswith("per_warp_active.pct"):
+            try:
+                res.append((float(vals[i].replace(",", "")), n))
+            except ValueError:
+                pass
+    return "\n".join(f"  {v:8.2f}  {n}" for v, n in sorted(res, reverse=True)[:20])
 
 
 if __name__ == "__main__":
@@ -63,4 +84,6 @@ if __name__ == "__main__":
                           "sm__inst_executed_pipe_tensor_op_hmma.avg.pct_of_peak_sustained_active",
                           "smsp__average_warp_latency_issue_stalled_barrier", "gpu__time_duration.sum"]).items():
         print(f"{k:40s} {v[0]:>14s} {v[1]}")
+    print("warp stall reasons (% of active warp cycles):")
+    print(stalls(rep))
     print(source(rep))
