@@ -179,6 +179,31 @@ tl_status tl_matmul_hostio(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t
                            const void* zeros, void* Y_dev, void* Y_host, void* workspace,
                            size_t workspace_bytes, uint32_t flags, void* stream);
 
+/* One matmul of a batched host-buffer call (tl_matmul_batch_hostio): the weight of one linear layer and
+ * its own batch M, as tl_matmul's arguments (device pointers). */
+typedef struct {
+  tl_wtype w;
+  int32_t group;
+  int64_t M, N, K;
+  const void* w_t;
+  const void* scales;
+  const void* zeros;        /* NULL unless uint with zero points */
+  void* workspace;          /* tl_matmul_workspace_bytes(w, a, M, N, K, group) bytes, zero-filled once; */
+  size_t workspace_bytes;   /* items may share one workspace (they run in stream order) */
+} tl_batch_item;
+
+/* End-to-end call for several matmuls whose activations arrive in ONE host buffer and whose outputs
+ * return in ONE host buffer (e.g. the linear layers of a decode step): one host->device copy of
+ * A_host (the items' A [M_i, K_i] row-major, concatenated in item order, each block starting at a
+ * multiple of 16 bytes -- automatic, since K % 128 == 0) into A_dev, the items' matmuls on `stream`
+ * in order (TL_PATH_AUTO, `flags` as tl_matmul_ex; consecutive decode launches overlap through
+ * programmatic dependent launch), Y_i into Y_dev (concatenated likewise), and one device->host copy
+ * of Y_dev into Y_host.  A_dev / Y_dev hold sum_i M_i K_i and sum_i M_i N_i elements of type `a`
+ * (int8 A for TL_ACT_I8).  No host synchronisation.  Errors as tl_matmul_ex for the first failing
+ * item (items before it are enqueued), TL_EINVAL_SHAPE for count < 0, TL_ENULL for NULL buffers. */
+tl_status tl_matmul_batch_hostio(tl_atype a, int32_t count, const tl_batch_item* items, const void* A_host,
+                                 void* A_dev, void* Y_dev, void* Y_host, uint32_t flags, void* stream);
+
 /* Which family (tl_path) and split-K grid (CTAs; 0 = the CUDA-core path's occupancy-sized grid)
  * tl_matmul would use for this problem on the current device (for the bench and the dispatch
  * sweep).  The rule is DESIGN.md "Dispatch". */

@@ -94,6 +94,15 @@ _tl_matmul_plan = _sig("tl_matmul_plan", ctypes.c_int,
 _tl_matmul_gathered = _sig("tl_matmul_gathered", ctypes.c_int,
                            [_W, _A, _i64, _i64, _i64, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _i64,
                             ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i32, _vp, _c_size, _u32, _vp])
+class tl_batch_item(ctypes.Structure):
+    _fields_ = [("w", tl_wtype), ("group", ctypes.c_int32), ("M", ctypes.c_int64), ("N", ctypes.c_int64),
+                ("K", ctypes.c_int64), ("w_t", ctypes.c_void_p), ("scales", ctypes.c_void_p),
+                ("zeros", ctypes.c_void_p), ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t)]
+
+
+_tl_matmul_batch_hostio = _sig("tl_matmul_batch_hostio", ctypes.c_int,
+                               [ctypes.c_int, ctypes.c_int32, ctypes.POINTER(tl_batch_item), _vp, _vp, _vp, _vp,
+                                _u32, _vp])
 _tl_gather_wait = _sig("tl_gather_wait", ctypes.c_int, [_vp, _i32, _i32, _u32, _vp])
 _tl_mx_scales_to_f16 = _sig("tl_mx_scales_to_f16", ctypes.c_int, [_vp, _i64, _i32, _vp, _vp])
 _tl_dequant = _sig("tl_dequant", ctypes.c_int, [_W, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _vp])
@@ -102,7 +111,7 @@ _tl_last_error = _sig("tl_last_error", ctypes.c_char_p, [])
 
 EXPORTED = ["tl_packed_bytes", "tl_transformed_bytes", "tl_format_version", "tl_pack", "tl_unpack",
             "tl_transform_weights", "tl_untransform_weights", "tl_matmul_workspace_bytes", "tl_matmul",
-            "tl_matmul_ex", "tl_matmul_hostio", "tl_matmul_plan", "tl_matmul_gathered", "tl_gather_wait", "tl_mx_scales_to_f16", "tl_dequant", "tl_status_str",
+            "tl_matmul_ex", "tl_matmul_hostio", "tl_matmul_batch_hostio", "tl_matmul_plan", "tl_matmul_gathered", "tl_gather_wait", "tl_mx_scales_to_f16", "tl_dequant", "tl_status_str",
             "tl_last_error"]
 
 
@@ -269,6 +278,25 @@ def tl_matmul_hostio(w: tl_wtype, M: int, N: int, K: int, group: int, A_host: to
     _check(_tl_matmul_hostio(w, _atype(A_dev), M, N, K, group, A_host.data_ptr(), _ptr(A_dev), _ptr(w_t),
                              _ptr(scales), _ptr(zeros), _ptr(Y_dev), Y_host.data_ptr(), _ptr(workspace),
                              workspace.numel(), flags, _stream(stream)), "tl_matmul_hostio")
+    return Y_host
+
+
+def batch_items(problems: list[dict]) -> "ctypes.Array":
+    """problems: dicts with w, group, M, N, K, w_t, scales, zeros (tensor or None), workspace (tensor)."""
+    arr = (tl_batch_item * max(len(problems), 1))()
+    for i, p in enumerate(problems):
+        arr[i] = tl_batch_item(p["w"], p["group"], p["M"], p["N"], p["K"], _ptr(p["w_t"]), _ptr(p["scales"]),
+                               _ptr(p.get("zeros")), _ptr(p["workspace"]), p["workspace"].numel())
+    return arr
+
+
+def tl_matmul_batch_hostio(items, count: int, A_host: torch.Tensor, A_dev: torch.Tensor, Y_dev: torch.Tensor,
+                           Y_host: torch.Tensor, atype: int = TL_ACT_F16, flags: int = 0, stream=None) -> torch.Tensor:
+    """One H2D of the concatenated activations, the items' matmuls in order, one D2H of the outputs."""
+    if A_host.is_cuda or Y_host.is_cuda:
+        raise ValueError("A_host / Y_host must be host tensors")
+    _check(_tl_matmul_batch_hostio(atype, count, items, A_host.data_ptr(), _ptr(A_dev), _ptr(Y_dev),
+                                   Y_host.data_ptr(), flags, _stream(stream)), "tl_matmul_batch_hostio")
     return Y_host
 
 

@@ -305,6 +305,40 @@ tl_status tl_matmul(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int
                       TL_PATH_AUTO, 0, 0u, stream);
 }
 
+tl_status tl_matmul_batch_hostio(tl_atype a, int32_t count, const tl_batch_item* items, const void* A_host,
+                                 void* A_dev, void* Y_dev, void* Y_host, uint32_t flags, void* stream) {
+  if (count < 0) return fail(TL_EINVAL_SHAPE, "count=%d < 0", count);
+  if (count == 0) return TL_OK;
+  if (a != TL_ACT_F16 && a != TL_ACT_BF16 && a != TL_ACT_I8)
+    return fail(TL_EUNSUPPORTED, "unknown activation type %d", (int)a);
+  if (!items || !A_host || !A_dev || !Y_dev || !Y_host) return fail(TL_ENULL, "tl_matmul_batch_hostio: NULL pointer");
+  const size_t ae = a == TL_ACT_I8 ? 1 : 2;
+  size_t a_bytes = 0, y_bytes = 0;
+  for (int i = 0; i < count; ++i) {
+    if (items[i].M < 0 || items[i].N <= 0 || items[i].K <= 0)
+      return fail(TL_EINVAL_SHAPE, "item %d: M=%lld N=%lld K=%lld", i, (long long)items[i].M, (long long)items[i].N,
+                  (long long)items[i].K);
+    a_bytes += (size_t)(items[i].M * items[i].K) * ae;
+    y_bytes += (size_t)(items[i].M * items[i].N) * 2;
+  }
+  cudaStream_t s = as_stream(stream);
+  if (cudaMemcpyAsync(A_dev, A_host, a_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return fail(TL_ECUDA, "H2D copy of the activations failed");
+  size_t ao = 0, yo = 0;
+  for (int i = 0; i < count; ++i) {
+    const tl_batch_item& it = items[i];
+    tl_status st = tl_matmul_ex(it.w, a, it.M, it.N, it.K, it.group, reinterpret_cast<uint8_t*>(A_dev) + ao, it.K,
+                                it.w_t, it.scales, it.zeros, reinterpret_cast<uint8_t*>(Y_dev) + yo, it.N, it.workspace,
+                                it.workspace_bytes, TL_PATH_AUTO, 0, flags, stream);
+    if (st != TL_OK) return st;
+    ao += (size_t)(it.M * it.K) * ae;
+    yo += (size_t)(it.M * it.N) * 2;
+  }
+  if (cudaMemcpyAsync(Y_host, Y_dev, y_bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return fail(TL_ECUDA, "D2H copy of the outputs failed");
+  return TL_OK;
+}
+
 tl_status tl_matmul_hostio(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64_t K, int32_t group,
                            const void* A_host, void* A_dev, const void* w_t, const void* scales, const void* zeros,
                            void* Y_dev, void* Y_host, void* workspace, size_t workspace_bytes, uint32_t flags,

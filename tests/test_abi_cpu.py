@@ -120,3 +120,18 @@ def test_wtype_grammar(lib):
     assert (lib.wtype("i5").kind, lib.wtype("i5").bits) == (1, 5)
     with pytest.raises(ValueError):
         lib.wtype("q4")
+
+
+def test_batch_hostio_argument_checks(lib):
+    L = lib._lib
+    items = (L.tl_batch_item * 1)()
+    st = L._tl_matmul_batch_hostio(0, -1, items, 16, 16, 16, 16, 0, None)
+    assert L._tl_status_str(st).decode() == "TL_EINVAL_SHAPE"
+    assert L._tl_matmul_batch_hostio(0, 0, None, None, None, None, None, 0, None) == 0  # empty batch: no-op
+    st = L._tl_matmul_batch_hostio(0, 1, items, None, 16, 16, 16, 0, None)
+    assert L._tl_status_str(st).decode() == "TL_ENULL"
+    st = L._tl_matmul_batch_hostio(9, 1, items, 16, 16, 16, 16, 0, None)
+    assert L._tl_status_str(st).decode() == "TL_EUNSUPPORTED"
+    items[0].M, items[0].N, items[0].K = 1, 0, 128
+    st = L._tl_matmul_batch_hostio(0, 1, items, 16, 16, 16, 16, 0, None)
+    assert L._tl_status_str(st).decode() == "TL_EINVAL_SHAPE"
