@@ -242,6 +242,23 @@ tl_status tl_matmul_gathered(tl_wtype w, tl_atype a, int64_t M, int64_t N, int64
  * TL_EINVAL_SHAPE unless 1 <= nranks <= 8 and 0 <= self < nranks; TL_ENULL for NULL flags. */
 tl_status tl_gather_wait(const uint32_t* flags, int32_t nranks, int32_t self, uint32_t epoch, void* stream);
 
+/* Row-parallel (K-sharded) variant of row f3.  Rank r holds the K rows [k0, k1) of the weight (k0, k1
+ * multiples of 128 and of the group) and computes, with tl_matmul on A[:, k0:k1], a PARTIAL
+ * P_r[M, N_total] = A[:, k0:k1] x dequant(W[k0:k1, :]) in the activation type.  After its matmul a
+ * rank calls tl_signal_peers (release +1, system scope, on flags_q[r] of every peer q, ordered after
+ * the stream's prior work); every rank then waits for the others (tl_gather_wait on its own flags)
+ * and reduces its column block [n0, n1) over NVLink:
+ *   Y[m, c] = fp16( sum_{q = 0 .. nranks-1} P_q[m, n0 + c] )  in fp32, in rank order (deterministic).
+ * parts[q] (HOST array of nranks device pointers, peer-mapped) = &P_q[0, n0], row stride ldp; Y =
+ * the rank's output block [M, N = n1 - n0] (row stride ldy).  N, ldp, ldy multiples of 8; pointers
+ * 16-byte aligned; a in {TL_ACT_F16, TL_ACT_BF16}.  The partials are rounded once to the activation
+ * type before the sum (reading R26).  The caller must not overwrite P_r for call e+1 before every
+ * peer has reduced call e (alternate two partial buffers).  Errors: TL_EINVAL_SHAPE, TL_ENULL,
+ * TL_EALIGN, TL_EUNSUPPORTED (other activation types). */
+tl_status tl_signal_peers(uint32_t* const* flag_peers, int32_t npeers, void* stream);
+tl_status tl_reduce_scatter_peer(tl_atype a, const void* const* parts, int32_t nranks, int64_t M, int64_t N,
+                                 int64_t ldp, void* Y, int64_t ldy, void* stream);
+
 /* Microscaling scales ("Microscaling data types can be thought as
  * a more fine-grained quantization thus we could also support it"; reading R25).  An MX weight is a
  * kernel format (fp4 e2m1, fp6 e2m3 / e3m2, fp8 e4m3, or int8 for MXINT8) with ONE E8M0 scale per

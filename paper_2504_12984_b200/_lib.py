@@ -103,6 +103,9 @@ class tl_batch_item(ctypes.Structure):
 _tl_matmul_batch_hostio = _sig("tl_matmul_batch_hostio", ctypes.c_int,
                                [ctypes.c_int, ctypes.c_int32, ctypes.POINTER(tl_batch_item), _vp, _vp, _vp, _vp,
                                 _u32, _vp])
+_tl_signal_peers = _sig("tl_signal_peers", ctypes.c_int, [ctypes.POINTER(_vp), _i32, _vp])
+_tl_reduce_scatter_peer = _sig("tl_reduce_scatter_peer", ctypes.c_int,
+                               [ctypes.c_int, ctypes.POINTER(_vp), _i32, _i64, _i64, _i64, _vp, _i64, _vp])
 _tl_gather_wait = _sig("tl_gather_wait", ctypes.c_int, [_vp, _i32, _i32, _u32, _vp])
 _tl_mx_scales_to_f16 = _sig("tl_mx_scales_to_f16", ctypes.c_int, [_vp, _i64, _i32, _vp, _vp])
 _tl_dequant = _sig("tl_dequant", ctypes.c_int, [_W, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _vp])
@@ -111,7 +114,7 @@ _tl_last_error = _sig("tl_last_error", ctypes.c_char_p, [])
 
 EXPORTED = ["tl_packed_bytes", "tl_transformed_bytes", "tl_format_version", "tl_pack", "tl_unpack",
             "tl_transform_weights", "tl_untransform_weights", "tl_matmul_workspace_bytes", "tl_matmul",
-            "tl_matmul_ex", "tl_matmul_hostio", "tl_matmul_batch_hostio", "tl_matmul_plan", "tl_matmul_gathered", "tl_gather_wait", "tl_mx_scales_to_f16", "tl_dequant", "tl_status_str",
+            "tl_matmul_ex", "tl_matmul_hostio", "tl_matmul_batch_hostio", "tl_matmul_plan", "tl_matmul_gathered", "tl_gather_wait", "tl_signal_peers", "tl_reduce_scatter_peer", "tl_mx_scales_to_f16", "tl_dequant", "tl_status_str",
             "tl_last_error"]
 
 
@@ -228,6 +231,24 @@ def tl_gather_wait(flags: torch.Tensor, nranks: int, rank: int, epoch: int, stre
     if flags.dtype not in (torch.int32, torch.uint32) or flags.numel() < nranks:
         raise ValueError("flags must be an int32/uint32 device tensor with nranks entries")
     _check(_tl_gather_wait(_ptr(flags), nranks, rank, epoch & 0xFFFFFFFF, _stream(stream)), "tl_gather_wait")
+
+
+def tl_signal_peers(flag_peers: list[int], stream=None) -> None:
+    """Row f3 (row-parallel): release +1 on every peer's flag slot for this rank after the stream's work."""
+    n = len(flag_peers)
+    fp = (_vp * max(n, 1))(*flag_peers)
+    _check(_tl_signal_peers(fp, n, _stream(stream)), "tl_signal_peers")
+
+
+def tl_reduce_scatter_peer(parts: list[int], M: int, N: int, ldp: int, Y: torch.Tensor, ldy: int | None = None,
+                           atype: int = TL_ACT_F16, stream=None) -> torch.Tensor:
+    """Row f3 (row-parallel): Y[M, N] = sum over ranks (rank order, fp32) of the partials at `parts`
+    (device addresses of each rank's partial at this rank's column block, row stride ldp)."""
+    n = len(parts)
+    pa = (_vp * max(n, 1))(*parts)
+    _check(_tl_reduce_scatter_peer(atype, pa, n, M, N, ldp, Y.data_ptr(), ldy if ldy is not None else N,
+                                   _stream(stream)), "tl_reduce_scatter_peer")
+    return Y
 
 
 def tl_mx_scales_to_f16(e8m0: torch.Tensor, exp_adjust: int = 0, out: torch.Tensor | None = None,

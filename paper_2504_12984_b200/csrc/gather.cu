@@ -69,3 +69,92 @@ extern "C" tl_status tl_gather_wait(const uint32_t* flags, int32_t nranks, int32
   gather_wait_kernel<<<1, 32, 0, as_stream(stream)>>>(flags, nranks, self, epoch, ms * 1000000ll);
   return check_launch("gather_wait_kernel");
 }
+
+// ---- row-parallel (K-sharded) variant: NVLink reduce-scatter over peer memory (row f3) ----------
+namespace tl {
+
+// One thread per pending signal: +1 (release, system scope) on every peer's arrival flag for this
+// rank, after all prior work of the stream (kernel boundary) -- "my partial is complete".
+__global__ void signal_peers_kernel(PeerOut po) {
+  if (threadIdx.x == 0) {
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    for (int i = 0; i < po.n; ++i) asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(po.flag[i]) : "memory");
+  }
+}
+
+// Y[m, c] = sum_{q = 0 .. P-1} parts[q][m, c] in fp32, in rank order (deterministic), rounded once;
+// 8 columns (16 bytes) per thread per row, grid-stride.  parts[q] are peer-mapped addresses of the
+// ranks' partials at this rank's column block (row stride ldp).
+template <bool BF>
+__global__ void __launch_bounds__(256) reduce_scatter_kernel(PeerParts pp, int M, int N, int64_t ldp,
+                                                             uint16_t* __restrict__ Y, int64_t ldy) {
+  const int vpr = N / 8;
+  const int64_t total = (int64_t)M * vpr;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / vpr;
+    const int v = (int)(i - m * vpr);
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+    for (int q = 0; q < pp.n; ++q) {
+      const uint4 x = __ldcv(reinterpret_cast<const uint4*>(pp.p[q] + m * ldp + (int64_t)v * 8));
+      const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        acc[2 * j] += Act<BF>::to_float((uint16_t)(w[j] & 0xFFFFu));
+        acc[2 * j + 1] += Act<BF>::to_float((uint16_t)(w[j] >> 16));
+      }
+    }
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      o[j] = (uint32_t)Act<BF>::from_float(acc[2 * j]) | ((uint32_t)Act<BF>::from_float(acc[2 * j + 1]) << 16);
+    *reinterpret_cast<uint4*>(Y + m * ldy + (int64_t)v * 8) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+}  // namespace tl
+
+extern "C" tl_status tl_signal_peers(uint32_t* const* flag_peers, int32_t npeers, void* stream) {
+  if (npeers < 0 || npeers > kMaxPeers) return fail(TL_EINVAL_SHAPE, "npeers=%d outside [0, %d]", npeers, kMaxPeers);
+  if (npeers == 0) return TL_OK;
+  if (!flag_peers) return fail(TL_ENULL, "tl_signal_peers: NULL flag array");
+  PeerOut po{};
+  for (int i = 0; i < npeers; ++i) {
+    if (!flag_peers[i]) return fail(TL_ENULL, "tl_signal_peers: NULL flag %d", i);
+    if (reinterpret_cast<uintptr_t>(flag_peers[i]) & 3u) return fail(TL_EALIGN, "flag %d not 4-byte aligned", i);
+    po.flag[i] = flag_peers[i];
+  }
+  po.n = npeers;
+  signal_peers_kernel<<<1, 32, 0, as_stream(stream)>>>(po);
+  return check_launch("signal_peers_kernel");
+}
+
+extern "C" tl_status tl_reduce_scatter_peer(tl_atype a, const void* const* parts, int32_t nranks, int64_t M,
+                                            int64_t N, int64_t ldp, void* Y, int64_t ldy, void* stream) {
+  if (a != TL_ACT_F16 && a != TL_ACT_BF16) return fail(TL_EUNSUPPORTED, "partials are fp16 or bf16 (atype %d)", (int)a);
+  if (nranks < 1 || nranks > kMaxPeers + 1) return fail(TL_EINVAL_SHAPE, "nranks=%d outside [1, %d]", nranks, kMaxPeers + 1);
+  if (M < 0 || N <= 0 || N % 8 || ldp < N || ldy < N || ldp % 8 || ldy % 8)
+    return fail(TL_EINVAL_SHAPE, "M=%lld N=%lld ldp=%lld ldy=%lld (N, ldp, ldy multiples of 8, ld >= N)",
+                (long long)M, (long long)N, (long long)ldp, (long long)ldy);
+  if (M == 0) return TL_OK;
+  if (!parts || !Y) return fail(TL_ENULL, "tl_reduce_scatter_peer: NULL pointer");
+  PeerParts pp{};
+  for (int q = 0; q < nranks; ++q) {
+    if (!parts[q]) return fail(TL_ENULL, "tl_reduce_scatter_peer: NULL partial %d", q);
+    if (!aligned16(parts[q])) return fail(TL_EALIGN, "partial %d not 16-byte aligned", q);
+    pp.p[q] = reinterpret_cast<const uint16_t*>(parts[q]);
+  }
+  pp.n = nranks;
+  if (!aligned16(Y)) return fail(TL_EALIGN, "Y not 16-byte aligned");
+  const int64_t vecs = M * (N / 8);
+  int blocks = (int)((vecs + 255) / 256);
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  if (a == TL_ACT_BF16)
+    reduce_scatter_kernel<true><<<blocks, 256, 0, as_stream(stream)>>>(pp, (int)M, (int)N, ldp,
+                                                                       reinterpret_cast<uint16_t*>(Y), ldy);
+  else
+    reduce_scatter_kernel<false><<<blocks, 256, 0, as_stream(stream)>>>(pp, (int)M, (int)N, ldp,
+                                                                        reinterpret_cast<uint16_t*>(Y), ldy);
+  return check_launch("reduce_scatter_kernel");
+}

@@ -21,6 +21,12 @@ struct PeerOut {
   int signal;                    // 1 on the launch that completes the call (tc2 chunks M by 128)
 };
 
+// row-parallel reduce-scatter: the ranks' partials at this rank's column block (peer-mapped)
+struct PeerParts {
+  const uint16_t* p[kMaxPeers + 1];
+  int n;
+};
+
 // Replicate one output element / 4 consecutive elements into every peer's gathered buffer.
 __device__ __forceinline__ void peer_store(const PeerOut& po, int64_t off, unsigned short v) {
   for (int i = 0; i < po.n; ++i) po.y[i][off] = v;

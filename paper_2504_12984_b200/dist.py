@@ -10,7 +10,9 @@ any torch.distributed backend works, the CPU tests use gloo), or -- row f3 -- no
 ``FusedGather`` maps every rank's gathered buffer into every other rank (CUDA IPC handles,
 exchanged once over the process group) and the matmul kernel's epilogue stores each finished
 element straight into all of them over NVLink (``tl_matmul_gathered``), then signals per-rank
-flags that the consumer waits on (``tl_gather_wait``).
+flags that the consumer waits on (``tl_gather_wait``).  The row-parallel (K-sharded) variant,
+``FusedReduceScatter``, sums the ranks' partials over NVLink with this library's reduce-scatter
+kernel (``tl_signal_peers`` / ``tl_gather_wait`` / ``tl_reduce_scatter_peer``) instead of NCCL.
 
 This module holds shard arithmetic and the collective only; every matmul runs in the
 CUDA library through ``_lib``.
@@ -110,6 +112,62 @@ class FusedGather:
         L.tl_matmul_gathered(layer.w, A.shape[0], layer.Ns, layer.K, layer.G, A, layer.w_t, layer.scales,
                              layer.zeros, Y[:, layer.n0:], self.N, ys, fs, layer._workspace(A.shape[0]))
         L.tl_gather_wait(self.flags, self.world, self.rank, self.epoch)
+        return Y
+
+
+def row_shard(K: int, world: int, rank: int, group: int) -> tuple[int, int]:
+    """Rows [k0, k1) of rank `rank` for the row-parallel (K-sharded) variant: contiguous, multiples
+    of lcm(128, group) so that no scale group and no 128-row tile straddles two ranks."""
+    import math
+    align = 128 * group // math.gcd(128, group)
+    if K % align:
+        raise ValueError(f"K={K} is not a multiple of lcm(128, group)={align}")
+    return column_shard(K, world, rank, align)
+
+
+def reduce_pointers(part_bases: list[int], n0: int, elem_bytes: int = 2) -> list[int]:
+    """Addresses tl_reduce_scatter_peer takes on a rank owning columns [n0, n1): every rank's partial
+    (base addresses as mapped in this process, row stride = the full N) at column n0."""
+    return [b + n0 * elem_bytes for b in part_bases]
+
+
+class FusedReduceScatter:
+    """Row f3, row-parallel: every rank's fp16 partial [M, N] (its K-slice's contribution) is mapped
+    into every other rank (CUDA IPC); after its matmul a rank signals the others, waits for them and
+    reduces its column block of all partials over NVLink (tl_reduce_scatter_peer, fixed rank order).
+    `nbuf` partial buffers alternate between calls."""
+
+    def __init__(self, M: int, N: int, world: int, rank: int, group=None, nbuf: int = 2, dtype=torch.float16):
+        from torch.multiprocessing.reductions import reduce_tensor
+        self.M, self.N, self.world, self.rank, self.nbuf = M, N, world, rank, nbuf
+        self.parts = [torch.empty((M, N), dtype=dtype, device="cuda") for _ in range(nbuf)]
+        self.flags = torch.zeros(world, dtype=torch.int32, device="cuda")
+        torch.cuda.synchronize()
+        mine = [reduce_tensor(t) for t in self.parts + [self.flags]]
+        self._peer_tensors = []
+        self.p_bases = [[0] * world for _ in range(nbuf)]
+        self.f_bases = [0] * world
+        for q, payload in enumerate(exchange(mine, world, group)):
+            ts = self.parts + [self.flags] if q == rank else [fn(*args) for fn, args in payload]
+            self._peer_tensors.append(ts)
+            for b in range(nbuf):
+                self.p_bases[b][q] = ts[b].data_ptr()
+            self.f_bases[q] = ts[nbuf].data_ptr()
+        self.n0, self.n1 = column_shard(N, world, rank)
+        self.epoch = 0
+
+    def __call__(self, w, K_shard: int, G: int, A_shard: torch.Tensor, w_t, scales, zeros, workspace,
+                 out: torch.Tensor | None = None) -> torch.Tensor:
+        """This rank's [M, n1-n0] block of sum_r A[:, K_r] x W[K_r, :]."""
+        self.epoch += 1
+        b = self.epoch % self.nbuf
+        P = self.parts[b]
+        L.tl_matmul(w, self.M, self.N, K_shard, G, A_shard, w_t, scales, zeros, P, workspace)
+        _, fs = peer_pointers([0] * self.world, self.f_bases, self.rank, 0)
+        L.tl_signal_peers(fs)
+        L.tl_gather_wait(self.flags, self.world, self.rank, self.epoch)
+        Y = out if out is not None else torch.empty((self.M, self.n1 - self.n0), dtype=P.dtype, device=P.device)
+        L.tl_reduce_scatter_peer(reduce_pointers(self.p_bases[b], self.n0), self.M, self.n1 - self.n0, self.N, Y)
         return Y
 
 

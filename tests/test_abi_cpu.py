@@ -135,3 +135,18 @@ def test_batch_hostio_argument_checks(lib):
     items[0].M, items[0].N, items[0].K = 1, 0, 128
     st = L._tl_matmul_batch_hostio(0, 1, items, 16, 16, 16, 16, 0, None)
     assert L._tl_status_str(st).decode() == "TL_EINVAL_SHAPE"
+
+
+def test_row_parallel_argument_checks(lib):
+    L = lib._lib
+    VP = L._vp * 8
+    st = lambda x: L._tl_status_str(x).decode()
+    assert st(L._tl_signal_peers(VP(*[16] * 8), 8, None)) == "TL_EINVAL_SHAPE"
+    assert st(L._tl_signal_peers(VP(18), 1, None)) == "TL_EALIGN"
+    assert L._tl_signal_peers(None, 0, None) == 0
+    assert st(L._tl_reduce_scatter_peer(2, VP(16, 32), 2, 1, 128, 128, 16, 128, None)) == "TL_EUNSUPPORTED"
+    assert st(L._tl_reduce_scatter_peer(0, VP(16, 32), 9, 1, 128, 128, 16, 128, None)) == "TL_EINVAL_SHAPE"
+    assert st(L._tl_reduce_scatter_peer(0, VP(16, 32), 2, 1, 100, 128, 16, 128, None)) == "TL_EINVAL_SHAPE"
+    assert st(L._tl_reduce_scatter_peer(0, VP(16, 32), 2, 1, 128, 64, 16, 128, None)) == "TL_EINVAL_SHAPE"
+    assert st(L._tl_reduce_scatter_peer(0, VP(16, 40), 2, 1, 128, 128, 16, 128, None)) == "TL_EALIGN"
+    assert L._tl_reduce_scatter_peer(0, VP(16, 32), 2, 0, 128, 128, 16, 128, None) == 0

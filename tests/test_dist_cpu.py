@@ -143,3 +143,57 @@ def _fused_worker(rank, world, port, M, N, out_dir):
 def test_fused_gather_peer_addresses(tmp_path, world):
     mp.spawn(_fused_worker, args=(world, _free_port(), 3, 1024, str(tmp_path)), nprocs=world, join=True)
     assert (tmp_path / "ok.npy").exists()
+
+
+def test_row_shard_and_reduce_pointers():
+    from paper_2504_12984_b200.dist import reduce_pointers, row_shard
+    K, G = 8192, 128
+    for world in (2, 3, 4, 8):
+        spans = [row_shard(K, world, r, G) for r in range(world)]
+        assert spans[0][0] == 0 and spans[-1][1] == K
+        assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+        assert all((k1 - k0) % 128 == 0 and k0 % G == 0 for k0, k1 in spans)
+    assert all(k0 % 384 == 0 for k0, _ in (row_shard(3 * 384 * 4, 4, r, 384) for r in range(4)))  # lcm(128, 384)
+    with pytest.raises(ValueError):
+        row_shard(8192 + 128, 2, 0, 256)
+    assert reduce_pointers([1000, 5000], 64) == [1128, 5128]
+
+
+def _rowpar_worker(rank, world, port, out_dir):
+    """Row-parallel host logic with gloo: every rank's partial is the oracle on its K rows; an
+    all_gather of the partials stands in for the peer mapping; each rank reduces its column block
+    in rank order in fp32 -- the concatenation must equal the same reduction done centrally."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import dequant, matmul_fp64, parse_wtype
+    from paper_2504_12984_b200.dist import column_shard, exchange, row_shard
+    fmt, M, K, N, G = "u4", 2, 1024, 512, 128
+    seed = wl.stable_seed("rowpar-cpu", fmt, M, K, N)
+    A = wl.gen_activations(M, K, seed)
+    codes = wl.gen_codes(fmt, K, N, seed)
+    s = wl.gen_scales(fmt, K, N, G, seed)
+    z = wl.gen_zeros(fmt, K, N, G, seed)
+    k0, k1 = row_shard(K, world, rank, G)
+    wd = dequant(parse_wtype(fmt), codes[k0:k1], s[k0 // G:k1 // G], z[k0 // G:k1 // G], G)
+    part = matmul_fp64(A[:, k0:k1], wd).astype(np.float16)
+    parts = exchange(part, world)
+    n0, n1 = column_shard(N, world, rank)
+    acc = np.zeros((M, n1 - n0), np.float32)
+    for p in parts:
+        acc = acc + p[:, n0:n1].astype(np.float32)
+    blocks = exchange(acc.astype(np.float16), world)
+    if rank == 0:
+        Y = np.concatenate(blocks, axis=1)
+        ref = np.zeros((M, N), np.float32)
+        for p in parts:
+            ref = ref + p.astype(np.float32)
+        assert np.array_equal(Y.view(np.uint16), ref.astype(np.float16).view(np.uint16))
+        np.save(os.path.join(out_dir, "ok.npy"), np.ones(1))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_row_parallel_two_ranks(tmp_path):
+    mp.spawn(_rowpar_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    assert (tmp_path / "ok.npy").exists()

@@ -112,3 +112,45 @@ def test_gathered_argument_checks(env):
     assert L._tl_status_str(L._tl_gather_wait(x.data_ptr(), 9, 0, 1, None)).decode() == "TL_EINVAL_SHAPE"
     assert L._tl_status_str(L._tl_gather_wait(x.data_ptr(), 2, 2, 1, None)).decode() == "TL_EINVAL_SHAPE"
     assert L._tl_gather_wait(x.data_ptr(), 1, 0, 1, None) == 0
+
+
+@pytest.mark.parametrize("world,M,fmt,K,N,G", [(2, 1, "u4", 1024, 512, 128), (4, 1, "i6", 2048, 1024, 128),
+                                              (3, 16, "f6e3m2", 1536, 768, 128), (2, 64, "u3", 1024, 256, 128),
+                                              (4, 3, "i3", 2048, 512, 256)])
+def test_row_parallel_reduce_scatter_virtual_ranks(env, world, M, fmt, K, N, G):
+    """Row-parallel: rank r computes the partial of its K rows; after every rank signalled, each rank
+    reduces its column block of all partials.  Bit-exact against the same fixed-order fp32 sum of
+    the fp16 partials done in numpy, and within O7 of the oracle."""
+    P, torch, dist = env
+    w = P.wtype(fmt)
+    A, codes, s, z = _problem(fmt, M, K, N, G, "rowpar")
+    parts = [torch.full((M, N), float("nan"), dtype=torch.float16, device="cuda") for _ in range(world)]
+    flags = [torch.zeros(world, dtype=torch.int32, device="cuda") for _ in range(world)]
+    for r in range(world):
+        k0, k1 = dist.row_shard(K, world, r, G)
+        _, _, wt = prepare_weights(P, torch, fmt, k1 - k0, N, np.ascontiguousarray(codes[k0:k1]))
+        ws = P.alloc_workspace(w, M, N, k1 - k0, G)
+        zr = None if z is None else to_dev(np.ascontiguousarray(z[k0 // G:k1 // G]), torch)
+        P.tl_matmul(w, M, N, k1 - k0, G, to_dev(np.ascontiguousarray(A[:, k0:k1]), torch), wt,
+                    to_dev(np.ascontiguousarray(s[k0 // G:k1 // G]), torch), zr, parts[r], ws)
+        _, fs = dist.peer_pointers([0] * world, [f.data_ptr() for f in flags], r, 0)
+        P.tl_signal_peers(fs)
+    ys = []
+    for r in range(world):
+        P.tl_gather_wait(flags[r], world, r, 1)
+        n0, n1 = dist.column_shard(N, world, r)
+        Y = torch.full((M, n1 - n0), float("nan"), dtype=torch.float16, device="cuda")
+        P.tl_reduce_scatter_peer(dist.reduce_pointers([p.data_ptr() for p in parts], n0), M, n1 - n0, N, Y)
+        ys.append(Y)
+    torch.cuda.synchronize()
+    for r in range(world):
+        f = flags[r].cpu().numpy()
+        assert f[r] == 0 and all(f[q] == 1 for q in range(world) if q != r), (r, f)
+    Yg = np.concatenate([y.cpu().numpy() for y in ys], axis=1)
+    ref = np.zeros((M, N), np.float32)
+    for p in parts:
+        ref = ref + p.cpu().numpy().astype(np.float32)       # rank order, fp32, one rounding
+    assert np.array_equal(Yg.view(np.uint16), ref.astype(np.float16).view(np.uint16))
+    wd = dequant(parse_wtype(fmt), codes, s, z, G)
+    rr = tolerance_check(Yg, matmul_fp64(A, wd), A, wd)
+    assert rr["ok"], rr
