@@ -386,6 +386,9 @@ def run_ours(args):
     # ---- north-star coverage: all 37 formats x 70B layers x M in {1, 16} (rank 0 only) ----
     spectrum = run_spectrum(args, P, torch, dev, peaks) if (rank == 0 and not args.no_spectrum) else None
 
+    # ---- row f4: int8 activations and MX weights (rank 0 only) ----
+    f4 = run_f4(args, P, torch, dev, peaks) if (rank == 0 and not args.no_spectrum) else None
+
     # ---- C5 (BASELINE configs[4]): Llama-3.3-70B gate_up strong-scaled over the ranks ----
     c5 = None if args.no_c5 else run_c5(args, P, torch, dist, world, rank, dev, peaks)
 
@@ -409,6 +412,7 @@ def run_ours(args):
             "details_extra_M": extra,
             "details_c5": c5,
             "details_spectrum": spectrum,
+            "details_f4": f4,
         }
         if world == 1 and not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline(args.formats, layers, G, M)
@@ -454,6 +458,70 @@ def run_spectrum(args, P, torch, dev, peaks):
                             "GBps": round(b / (us * 1e-6) / 1e9, 1),
                             "hbm_frac": round(b / (us * 1e-6) / 1e9 / peaks["hbm_gbs"], 3)})
             del wt, s, z, ws
+    return out
+
+
+def run_f4(args, P, torch, dev, peaks):
+    """SURVEY §8(f) row f4 measured on the 70B layers at M = 1 and 16 (one tl_matmul per (case, layer, M),
+    10 back-to-back launches after 3 warm-ups, device time):
+      * int8 activations (TL_ACT_I8; u3 / i5 / f6e3m2 / u8 weights, G = 128): the staging kernel plus
+        the fp16 path; algorithmic bytes count A at one byte per element;
+      * MX weights (group 32 with E8M0 scales converted once by tl_mx_scales_to_f16): fp4 e2m1,
+        fp6 e2m3, fp6 e3m2, fp8 e4m3 and MXINT8 (int8 x 2^-6); algorithmic bytes = codes + one fp16
+        scale per 32 weights + A + Y."""
+    out = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def clock(fn):
+        for _ in range(3):
+            fn()
+        e0.record()
+        for _ in range(10):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / 10 * 1e3
+
+    for lname in ("qkv", "gate_up"):
+        K, N = wl.LLAMA33_70B[lname]
+        for fmt in ("u3", "i5", "f6e3m2", "u8"):
+            G = 128
+            w = P.wtype(fmt)
+            seed = wl.stable_seed("f4-a8", fmt, lname)
+            wt = P.tl_transform_weights(w, K, N, P.tl_pack(w, K, N, wl.gen_codes_torch(fmt, K, N, seed, dev)))
+            s = wl.gen_scales_torch(fmt, K, N, G, seed, dev)
+            z = wl.gen_zeros_torch(fmt, K, N, G, seed, dev)
+            for M in (1, 16):
+                ws = torch.zeros(P.tl_matmul_workspace_bytes(w, M, N, K, G, P.TL_ACT_I8), dtype=torch.uint8,
+                                 device=dev)
+                A8 = torch.randint(-128, 128, (M, K), dtype=torch.int8, device=dev)
+                Y = torch.empty((M, N), dtype=torch.float16, device=dev)
+                us = clock(lambda: P.tl_matmul_ex(w, M, N, K, G, A8, wt, s, z, Y, ws, flags=P.TL_FLAG_STATIC_WEIGHTS))
+                b = alg_bytes(fmt, M, K, N, G) - M * K
+                out.append({"case": "a8", "fmt": fmt, "layer": lname, "M": M, "us": round(us, 2),
+                            "GBps": round(b / (us * 1e-6) / 1e9, 1),
+                            "hbm_frac": round(b / (us * 1e-6) / 1e9 / peaks["hbm_gbs"], 3)})
+            del wt, s, z
+        for name, fmt, adj, center in (("mxfp4", "f4e2m1", 0, 119), ("mxfp6_e2m3", "f6e2m3", 0, 120),
+                                       ("mxfp6_e3m2", "f6e3m2", 0, 117), ("mxfp8_e4m3", "f8e4m3", 0, 115),
+                                       ("mxint8", "i8", -6, 121)):
+            G = 32
+            w = P.wtype(fmt)
+            seed = wl.stable_seed("f4-mx", fmt, lname)
+            wt = P.tl_transform_weights(w, K, N, P.tl_pack(w, K, N, wl.gen_codes_torch(fmt, K, N, seed, dev)))
+            e8 = torch.randint(center - 3, center + 4, (K // G, N), dtype=torch.int32, device=dev).to(torch.uint8)
+            s = P.tl_mx_scales_to_f16(e8, adj)
+            for M in (1, 16):
+                ws = torch.zeros(P.tl_matmul_workspace_bytes(w, M, N, K, G), dtype=torch.uint8, device=dev)
+                A = wl.gen_activations_torch(M, K, seed, dev)
+                Y = torch.empty((M, N), dtype=torch.float16, device=dev)
+                us = clock(lambda: P.tl_matmul_ex(w, M, N, K, G, A, wt, s, None, Y, ws, flags=P.TL_FLAG_STATIC_WEIGHTS))
+                b = alg_bytes(fmt, M, K, N, G)
+                path, _ = P.tl_matmul_plan(w, M, N, K, G)
+                out.append({"case": name, "fmt": fmt, "layer": lname, "M": M, "us": round(us, 2),
+                            "GBps": round(b / (us * 1e-6) / 1e9, 1),
+                            "hbm_frac": round(b / (us * 1e-6) / 1e9 / peaks["hbm_gbs"], 3), "path": path})
+            del wt, s
     return out
 
 
