@@ -63,7 +63,7 @@ struct TcdParams {
                    // (LOP3 takes one immediate; the magic must live in a register)
   int static_w;  // TL_FLAG_STATIC_WEIGHTS: the weight stream may start before griddepcontrol.wait
   PeerOut po;  // row f3: gathered output fused into the epilogue (peer.cuh); po.n == 0: local only
-  int dbg;  // experiment knobs (TL_TCD_DBG; device-side ones only with -DTCD_TRACE): 1 skip MMAs,
+  int dbg;  // experiment knobs (TL_TCD_DBG; device-side ones only with -DTCD_TRACE): 1 skip MMAs, 16 skip fixups, 64 stream only,
             // 4 skip unpack/STTM, 8 skip scale/zero copies, 128 no PDL (host)
 };
 
@@ -95,7 +95,13 @@ struct TcdCfg {
   // activation operand ring: slot t % NOP is refilled once MMA(t - NOP) completed, so the
   // operand of tile t is in flight for NOP tiles (an L2 round trip); NOP <= NACC keeps the
   // completion-barrier parity unambiguous
-  static constexpr int NOP = 8;
+  // decode: NOP slots; with 16, slot t % 16 always holds row t % 16 (never zeroed again).  Measured
+  // 8 vs 16: the same time on every 70B layer (DESIGN.md §6 experiments), so the default keeps the
+  // smaller ring (32 KB more for weight stages).
+#ifndef TCD_NOP_ROT
+#define TCD_NOP_ROT 8
+#endif
+  static constexpr int NOP = kRot ? TCD_NOP_ROT : 8;
   static_assert(NOP <= NACC, "operand ring vs completion ring");
   static_assert(AccCol + (kRot ? 32 : NACC * 16) <= 512, "TMEM split");
   static_assert(NACC % 4 == 0 && Lag >= 1 && Lag <= 2 && 4 * Lag < NACC, "fixup lag");
@@ -104,7 +110,7 @@ constexpr int kTcdMaxNW = 7, kTcdMaxNACC = 16;  // shared-memory sizing of the b
 constexpr int kTcdThreads = 128 + kTcdNG * 128;
 constexpr int kTcdNB = 16;                      // MMA N (batch rows, zero-padded)
 constexpr uint32_t kTcdOpBytes = kTcdNB * 256;  // 16 rows x 128 k fp16, two 64-k SW128 blocks
-constexpr int kTcdMaxNOP = 8;                   // activation operand ring slots (max over configs)
+constexpr int kTcdMaxNOP = 16;                  // activation operand ring slots (max over configs)
 
 __device__ __forceinline__ void tcd_sttm_x16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(
@@ -186,7 +192,10 @@ __device__ __forceinline__ void tcd_istamp(const TcdParams& p, int dw, int lane,
 
 // tiles per weight stage: ~12 KB of packed weights per stage (the cp.async.bulk ring streams at
 // full HBM rate only with stages of ~12 KB and more, tools/tma_probe.cu)
-__host__ __device__ constexpr int tcd_tiles_per_stage(int b) { return (6 + b - 1) / b; }
+#ifndef TCD_STAGE_UNITS
+#define TCD_STAGE_UNITS 6
+#endif
+__host__ __device__ constexpr int tcd_tiles_per_stage(int b) { return (TCD_STAGE_UNITS + b - 1) / b; }
 
 template <class F, int MT, bool BF>
 __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_constant__ CUtensorMap tmapA, TcdParams p) {
@@ -307,7 +316,10 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
         constexpr int R = kR;
         for (int t0 = 0, q = 0; t0 < T; t0 += R, ++q) {
           const int n_t = min(R, T - t0);
-          if (q >= NS) mbar_wait_sleepy(&empty_tma[s], ph ^ 1);
+          if (q >= NS) {
+            if (TCD_TRACE_ON && (p.dbg & 512)) mbar_wait(&empty_tma[s], ph ^ 1);
+            else mbar_wait_sleepy(&empty_tma[s], ph ^ 1);
+          }
           if (t0 < 64) tcd_tstamp(p, 2720 + t0);
           const uint32_t st = st_u + s * SB, bar = bar0 + 8 * s;
           mbar_arrive_expect_tx_u32(bar, (uint32_t)n_t * WB);
@@ -350,13 +362,14 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
         const int kb = lane >> 4, c = (lane & 15) >> 1, half = lane & 1;
         int kt = u0 - (u0 / KT) * KT;
         int o = 0;
-        for (int t = 0; t < T; ++t) {
+        for (int t = 0; t < ((TCD_TRACE_ON && (p.dbg & 64)) ? 0 : T); ++t) {
           if (t >= kTcdNOP) mbar_wait(&full_acc[(t - kTcdNOP) % NACC], (uint32_t)((t - kTcdNOP) / NACC) & 1);
           const uint2 v = *reinterpret_cast<const uint2*>(stash + kt * 256 + lane * 8);
           const int r = t & 15, rz = (t + 8) & 15;
           uint8_t* slot = smem + p.op_off + o * kTcdOpBytes + kb * (kTcdNB * 128);
           *reinterpret_cast<uint2*>(slot + r * 128 + ((c ^ (r & 7)) << 4) + half * 8) = v;
-          *reinterpret_cast<uint2*>(slot + rz * 128 + ((c ^ (rz & 7)) << 4) + half * 8) = make_uint2(0u, 0u);
+          if constexpr (kTcdNOP != 16)  // with 16 slots, slot t % 16 only ever holds row t % 16
+            *reinterpret_cast<uint2*>(slot + rz * 128 + ((c ^ (rz & 7)) << 4) + half * 8) = make_uint2(0u, 0u);
           fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core (async proxy)
           __syncwarp();
           if (lane == 0) mbar_arrive(&full_op[o]);
@@ -369,7 +382,7 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
     // ------------------------------ MMA issuer (one thread) ------------------------------
     // the dequant group has already seen the tile's activation operand land (full_op) before it
     // arrives on full_w, so the issuer waits only for the W^T slot and the accumulator
-    if (elect_one()) {
+    if (!(TCD_TRACE_ON && (p.dbg & 64)) && elect_one()) {
       const uint32_t idesc =
           (1u << 4) | Act<BF>::idesc_ab | ((uint32_t)(kTcdNB >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
       int o = 0, g = 0, a = 0;
@@ -416,11 +429,16 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
     int s = 0;
     uint32_t ph = 0;
     for (int t = 0, j = 0; t < T; ++t) {
-      if (j == 0 && t >= NS * kR) mbar_wait_sleepy(&empty_tma[s], ph ^ 1);
+      if (j == 0 && t >= NS * kR) {
+        if (TCD_TRACE_ON && (p.dbg & 512)) mbar_wait(&empty_tma[s], ph ^ 1);  // 512: spinning waits
+        else mbar_wait_sleepy(&empty_tma[s], ph ^ 1);
+      }
       const uint32_t side = st_u + s * SB + kR * WB + 256 * j + 8 * lane;
       const int64_t off = (int64_t)growf * p.N + (int64_t)ntf * kBN + 4 * lane;
-      cp_async_8(side, p.scales + off);
-      if (has_zeros) cp_async_8(side + kR * 256, p.zeros + off);
+      if (!(TCD_TRACE_ON && (p.dbg & 256))) {  // 256: timing experiment, no scale / zero copies
+        cp_async_8(side, p.scales + off);
+        if (has_zeros) cp_async_8(side + kR * 256, p.zeros + off);
+      }
       if (++ktf == KT) {
         ktf = 0;
         ++ntf;
@@ -454,6 +472,7 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
     for (int m = 0; m < MT; ++m) tot[m] = 0.f;
 
     auto fixup = [&](int tp, float c1) {
+      if (TCD_TRACE_ON && (p.dbg & 16)) return;  // timing experiment: no fixups (results invalid)
       const int a = tp % NACC;
       mbar_wait(&full_acc[a], (uint32_t)(tp / NACC) & 1);
       tc_fence_after();
@@ -493,6 +512,18 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
       for (; t < t1; t += NG, ++kk) {
         tcd_istamp(p, dw, lane, kk, 0);
         mbar_wait(&full_tma[s], ph);
+        if (TCD_TRACE_ON && (p.dbg & 64)) {  // timing experiment: stream only (results invalid)
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty_tma[s]);
+          const int qn = (t + NG) / kR;
+          s += qn - qst;
+          qst = qn;
+          while (s >= NS) {
+            s -= NS;
+            ph ^= 1;
+          }
+          continue;
+        }
         tcd_istamp(p, dw, lane, kk, 1);
         if (kk == 0 && dw == 0 && lane == 0) tcd_stamp(p, 4);
         const int jt = t - qst * kR;  // tile within the stage
