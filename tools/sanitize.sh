@@ -21,3 +21,12 @@ u4 1024 512 1 1 5
 i3 1024 512 3 1 5
 LIST
 cat $OUT
+# round-2 paths: int8 activations, MX, gathered epilogue, row-parallel reduce-scatter, batched host I/O
+# (not run this round: compute-sanitizer was closed on the GPU pool after the first pass; the script
+# tools/run_new_paths.py alone checks each path against the oracle)
+for tool in memcheck racecheck synccheck; do
+  echo "== $tool tools/run_new_paths.py" >> $OUT
+  timeout -s KILL 600 compute-sanitizer --tool $tool --print-limit 5 python tools/run_new_paths.py 2>&1 \
+    | grep -E "ERROR SUMMARY|RACECHECK SUMMARY|Error|error|hazard| ok |FAIL" | head -16 >> $OUT
+done
+cat $OUT
