@@ -1,6 +1,7 @@
-// tc.cu -- host side of the tensor-core path: shared-memory carve-up, the TMA tensor map
-// of the activations, m-chunking (MMA N <= 256) and the per-format dispatch.  The kernel
-// (tc.cuh) is instantiated one format per translation unit (build/gen/tc_*.cu).
+// tc.cu -- host side of the tensor-core paths (decode tcd.cuh, batched tc2.cuh): shared-memory
+// carve-up, the TMA tensor map of the activations, m-chunking (MMA N <= 128) and the per-format
+// dispatch.  The kernels are instantiated one format per translation unit (build/gen/tcd_*.cu,
+// build/gen/tc2_*.cu).
 #include <cudaTypedefs.h>
 
 #include <cstdlib>

@@ -17,13 +17,15 @@
 //  * the group scale is applied once per (tile, column, batch row) in fp32:
 //        Y[m,n] += s[g,n] * D[n,m]      (floats: s[g,n] * 2^(15-bias) * D[n,m]).
 //
-// The packed weight tile (2048*b B) and its scale and zero-point row slices (256 B each) arrive in
-// ONE TMA ring stage (cp.async.bulk, PAPER.md:148-151 step (1)); the activation operand has its
-// own ring.  Roles (128 + 128*NG threads):
+// A ring stage holds R consecutive packed weight tiles (2048*b B each, ONE cp.async.bulk,
+// PAPER.md:148-151 step (1)) and their scale and zero-point row slices (256 B each, 8-byte cp.async
+// by warp 3 completing on the same stage barrier); the activation operand has its own ring.
+// Roles (128 + 128*NG threads):
 //   warp 0       weight-stream TMA producer (one elected thread)
 //   warp 1       TMEM allocator + MMA issuer (one elected thread)
-//   warp 2       activation-operand TMA producer (one elected thread; 2-D tensor map)
-//   warp 3       idle (keeps the dequant warps aligned to TMEM lane quarters)
+//   warp 2       activation operand: M > 1 a TMA producer (2-D tensor map); M = 1 the operand
+//                WRITER (A[0, :] resident in shared memory, one row per tile, see TcdCfg)
+//   warp 3       scale / zero stager (cp.async into the stage's side area)
 //   warps 4..    NG dequant groups of 4 warps (warp%4 = TMEM lane quarter = 32 columns); group
 //                g handles tiles t = g, g+NG, ... of the CTA's stream-K range: unpack into its
 //                W^T slot, hand it to the MMA, then -- TcdCfg::Lag group-iterations late, so it never
