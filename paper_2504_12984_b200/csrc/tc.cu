@@ -83,7 +83,7 @@ tl_status tcd_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, con
   const int R = tcd_tiles_per_stage(w.bits);
   p.R = R;
   p.stage_bytes = ((uint32_t)R * (wb + 512) + 127) & ~127u;  // R weight tiles | R scale rows | R zero rows
-  const uint32_t red = (uint32_t)kTcdNG * (uint32_t)M * kBN * 4;
+  const uint32_t red = (uint32_t)((M <= 1 && K * 2 <= 65536) ? TcdCfg<1>::NG : TcdCfg<kTcdNB>::NG) * (uint32_t)M * kBN * 4;
   const uint32_t opb = (uint32_t)((M <= 1 && K * 2 <= 65536) ? TcdCfg<1>::NOP : TcdCfg<kTcdNB>::NOP) * kTcdOpBytes;
   const uint32_t stash = p.rot ? (uint32_t)(K * 2) : 0u;
   const uint64_t fixed = 1024 /*align*/ + (uint64_t)opb + stash + red + 2048 /*barriers, tmem slot, flags*/;

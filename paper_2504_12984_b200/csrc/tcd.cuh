@@ -90,7 +90,12 @@ struct TcdCfg {
 #ifndef TCD_NW_ROT
 #define TCD_NW_ROT 5
 #endif
-  static constexpr int NW = kRot ? TCD_NW_ROT : 5;       // W^T slots
+#ifndef TCD_NG_ROT
+#define TCD_NG_ROT 4
+#endif
+  static constexpr int NG = kRot ? TCD_NG_ROT : 4;       // dequant groups of 4 warps
+  static constexpr int Threads = 128 + NG * 128;
+  static constexpr int NW = kRot ? (TCD_NW_ROT > NG ? TCD_NW_ROT : NG + 1) : 5;  // W^T slots
   static constexpr int NACC = kRot ? 16 : 12;            // completion barriers (= accumulators if !kRot)
   static constexpr int Lag = kRot ? 2 : NACC / 4 - 1;    // fixup lag (group iterations)
   static constexpr uint32_t AccCol = 64 * NW;            // first accumulator column
@@ -106,7 +111,8 @@ struct TcdCfg {
   static constexpr int NOP = kRot ? TCD_NOP_ROT : 8;
   static_assert(NOP <= NACC, "operand ring vs completion ring");
   static_assert(AccCol + (kRot ? 32 : NACC * 16) <= 512, "TMEM split");
-  static_assert(NACC % 4 == 0 && Lag >= 1 && Lag <= 2 && 4 * Lag < NACC, "fixup lag");
+  static_assert(NACC % 4 == 0 && Lag >= 1 && Lag <= 2 && NG * Lag < NACC, "fixup lag");
+  static_assert(kRot || NACC % NG == 0, "per-tile accumulators: the fixup of tile t - NACC is its group's");
 };
 constexpr int kTcdMaxNW = 7, kTcdMaxNACC = 16;  // shared-memory sizing of the barrier arrays
 constexpr int kTcdThreads = 128 + kTcdNG * 128;
@@ -200,14 +206,14 @@ __device__ __forceinline__ void tcd_istamp(const TcdParams& p, int dw, int lane,
 __host__ __device__ constexpr int tcd_tiles_per_stage(int b) { return (TCD_STAGE_UNITS + b - 1) / b; }
 
 template <class F, int MT, bool BF>
-__global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_constant__ CUtensorMap tmapA, TcdParams p) {
+__global__ void __launch_bounds__(TcdCfg<MT>::Threads, 1) tcd_kernel(const __grid_constant__ CUtensorMap tmapA, TcdParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr bool kInt = F::kind != kFloat;  // integer codes: magic form + HFMA2 (u - z)
   constexpr uint32_t WB = tile_bytes(F::bits);
   constexpr int kR = tcd_tiles_per_stage(F::bits);
   using Cfg = TcdCfg<MT>;
-  constexpr int NG = kTcdNG, NACC = Cfg::NACC, kTcdNW = Cfg::NW;
+  constexpr int NG = Cfg::NG, NACC = Cfg::NACC, kTcdNW = Cfg::NW;
   constexpr uint32_t kTcdAccCol = Cfg::AccCol;
   constexpr int kTcdNOP = Cfg::NOP;
   const int NS = p.ns;
@@ -270,7 +276,7 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
   if constexpr (Cfg::kRot) {
     // decode: every operand row starts at zero; the writer only ever touches one row per tile
     uint4* z = reinterpret_cast<uint4*>(smem + p.op_off);
-    for (int i = threadIdx.x; i < kTcdNOP * (int)kTcdOpBytes / 16; i += kTcdThreads) z[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int i = threadIdx.x; i < kTcdNOP * (int)kTcdOpBytes / 16; i += Cfg::Threads) z[i] = make_uint4(0u, 0u, 0u, 0u);
     fence_proxy_async_smem();
   }
   const uint32_t op_u = st_u + p.op_off;
@@ -699,11 +705,11 @@ __global__ void __launch_bounds__(kTcdThreads, 1) tcd_kernel(const __grid_consta
 
 template <class F, int MT, bool BF>
 tl_status launch_tcd_mt(const TcdParams& p, const CUtensorMap* tmap, int grid, uint32_t smem_bytes, cudaStream_t st) {
-  if (prepare_kernel(reinterpret_cast<const void*>(tcd_kernel<F, MT, BF>), 227 * 1024, kTcdThreads) == 0)
+  if (prepare_kernel(reinterpret_cast<const void*>(tcd_kernel<F, MT, BF>), 227 * 1024, TcdCfg<MT>::Threads) == 0)
     return fail(TL_ECUDA, "tcd_kernel: %s", tl_last_error());
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kTcdThreads);
+  cfg.blockDim = dim3(TcdCfg<MT>::Threads);
   cfg.dynamicSmemBytes = smem_bytes;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
