@@ -244,6 +244,18 @@ tl_status tc_matmul(tl_wtype w, int64_t M, int64_t N, int64_t K, int32_t G, cons
     int grid = grid_req > 0 ? grid_req : splitk_grid((p.NT + 1) / 2, sms, true);
     if (grid > kTcMaxCtas) grid = kTcMaxCtas;
     if (grid > p.units) grid = p.units;
+    // distributed stream-K reduction (tc2.cuh): only for the aligned splits (grid = S x n-pairs, so
+    // every CTA's range lies inside one n-pair and its S contributors start together) and when every
+    // CTA is resident at once (one CTA per SM).  Measured: u3 M = 128 qkv 42.6 -> 39.9 us, o 37.9 ->
+    // 33.7, down 69.3 -> 64.2; with unaligned ranges the contributors' waits chain (148 CTAs on qkv:
+    // 57 -> 223 us), hence the guard.  TL_TC2_DIST=0 keeps the last-arriver reduction.
+    {
+      int sm_count = 148;
+      cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
+      const char* d = getenv("TL_TC2_DIST");
+      const int npairs = (p.NT + 1) / 2;
+      p.dist = (grid <= sm_count && grid % npairs == 0 && (d == nullptr || atoi(d) != 0)) ? 1 : 0;
+    }
     s = TL_EUNSUPPORTED;
     dispatch_format(w.kind, w.bits, w.kind == 2 ? w.exp_bits : 0, [&](auto f) {
       using F = decltype(f);

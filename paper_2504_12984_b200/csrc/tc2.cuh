@@ -47,6 +47,8 @@ struct Tc2Params {
   int* sem;        // [n-pairs]
   uint32_t magic;  // 0x64006400 (a kernel argument: the LOP3 takes one immediate, see tcd)
   int bf;          // 1: bf16 activations / scales / zeros / Y
+  int dist;        // 1: distributed stream-K reduction (every contributor reduces 1/S of the tile; needs
+                   //    all CTAs resident: grid <= SMs)
   PeerOut po;      // row f3: gathered output fused into the epilogue (peer.cuh); po.n == 0: local only
   int dbg;         // TL_TC2_DBG timing experiments (results invalid): 1 skip partial stores, 2 skip reduction
 };
@@ -397,8 +399,21 @@ __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_consta
         if (threadIdx.x == 64) {
           const int lo = (int)((((int64_t)ua + 1) * grid - 1) / p.units);
           const int hi = (int)((((int64_t)ub) * grid - 1) / p.units);
-          const int prev = atomicAdd(&p.sem[np], 1);
-          flag[0] = (prev == hi - lo) ? 1 : 0;
+          if (p.dist) {
+            // distributed: publish, then wait for every contributor's partial (all CTAs of the grid
+            // are resident, so the wait cannot block a contributor from running)
+            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(&p.sem[np]) : "memory");
+            for (;;) {
+              int v;
+              asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(&p.sem[np]) : "memory");
+              if (v >= hi - lo + 1) break;
+              __nanosleep(32);
+            }
+            flag[0] = 1;
+          } else {
+            const int prev = atomicAdd(&p.sem[np], 1);
+            flag[0] = (prev == hi - lo) ? 1 : 0;
+          }
           flag[1] = lo;
           flag[2] = hi;
           flag[3] = ((int)((int64_t)lo * p.units / grid) / KT == np) ? 0 : 1;
@@ -413,10 +428,13 @@ __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_consta
           const int lo = flag[1], hi = flag[2];
           const int64_t sstride = (int64_t)2 * NB * kBN;
           const int tid = threadIdx.x - 64;
-          const int nv = p.M * (kBN / 4);  // float4 per tile
+          const int nvt = p.M * (kBN / 4);  // float4 per tile
+          // distributed: contributor ci of S reduces elements [ci*nvt/S, (ci+1)*nvt/S) of each tile
+          const int S = hi - lo + 1, ci = p.dist ? cta - lo : 0, SS = p.dist ? S : 1;
+          const int ebeg = (int)((int64_t)ci * nvt / SS), nv = (int)((int64_t)(ci + 1) * nvt / SS);
           for (int tj = 0; tj < (two ? 2 : 1); ++tj) {
             const float* pb = p.partial + (int64_t)tj * NB * kBN;
-            for (int e0 = tid; e0 < nv; e0 += 4 * kTc2Groups * 128) {
+            for (int e0 = ebeg + tid; e0 < nv; e0 += 4 * kTc2Groups * 128) {
               float4 acc[4];
 #pragma unroll
               for (int j = 0; j < 4; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -460,7 +478,16 @@ __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_consta
             }
           }
         }
-        if (flag[0] && threadIdx.x == 64) p.sem[np] = 0;
+        if (p.dist) {
+          // second arrival after the slice: the last of the 2S resets the semaphore
+          named_bar_sync(1, kTc2Groups * 128);
+          if (threadIdx.x == 64) {
+            const int S2 = 2 * (flag[2] - flag[1] + 1);
+            if (atomicAdd(&p.sem[np], 1) == S2 - 1) p.sem[np] = 0;
+          }
+        } else if (flag[0] && threadIdx.x == 64) {
+          p.sem[np] = 0;
+        }
         named_bar_sync(1, kTc2Groups * 128);
       }
       ++seg;
