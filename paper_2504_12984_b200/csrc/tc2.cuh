@@ -505,7 +505,24 @@ tl_status launch_tc2(const Tc2Params& p, const CUtensorMap* tmap, int grid, uint
   auto go = [&](auto kern) -> tl_status {
     if (prepare_kernel(reinterpret_cast<const void*>(kern), 227 * 1024, kTc2Threads) == 0)
       return fail(TL_ECUDA, "tc2_kernel: %s", tl_last_error());
-    kern<<<grid, kTc2Threads, smem_bytes, st>>>(*tmap, p);
+    if (!p.dist) {
+      kern<<<grid, kTc2Threads, smem_bytes, st>>>(*tmap, p);
+      return TL_OK;
+    }
+    // the distributed reduction waits for sibling CTAs: a cooperative launch guarantees that every
+    // CTA of the grid is resident at once (no deadlock even with other kernels on other streams)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kTc2Threads);
+    cfg.dynamicSmemBytes = smem_bytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, *tmap, p);
+    if (e != cudaSuccess) return fail(TL_ECUDA, "tc2_kernel cooperative launch: %s", cudaGetErrorString(e));
     return TL_OK;
   };
   tl_status r;
