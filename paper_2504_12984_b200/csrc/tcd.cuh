@@ -65,7 +65,7 @@ struct TcdParams {
                    // (LOP3 takes one immediate; the magic must live in a register)
   int static_w;  // TL_FLAG_STATIC_WEIGHTS: the weight stream may start before griddepcontrol.wait
   PeerOut po;  // row f3: gathered output fused into the epilogue (peer.cuh); po.n == 0: local only
-  int dbg;  // experiment knobs (TL_TCD_DBG; device-side ones only with -DTCD_TRACE): 1 skip MMAs, 16 skip fixups, 64 stream only,
+  int dbg;  // experiment knobs (TL_TCD_DBG; device-side ones only with -DTCD_TRACE): 1 skip MMAs, 16 skip fixups, 64 stream only, 1024 no scale stager,
             // 4 skip unpack/STTM, 8 skip scale/zero copies, 128 no PDL (host)
 };
 
@@ -251,7 +251,8 @@ __global__ void __launch_bounds__(TcdCfg<MT>::Threads, 1) tcd_kernel(const __gri
     tcd_stamp(p, 0);
     if (TCD_TRACE_ON && p.trace) p.trace[blockIdx.x * 16 + 10] = T;
     for (int s = 0; s < NS; ++s) {
-      mbar_init(&full_tma[s], 1 + 32);   // the weight TMA (arrive + tx) and warp 3's 32 cp.async lanes
+      // the weight TMA (arrive + tx) and warp 3's 32 cp.async lanes (1024: timing experiment, no stager)
+      mbar_init(&full_tma[s], (TCD_TRACE_ON && (p.dbg & 1024)) ? 1 : 1 + 32);
       mbar_init(&empty_tma[s], 4 * kR);  // every tile of the stage: its group's 4 warps
     }
     mbar_init(stash_bar, 1);
@@ -426,6 +427,9 @@ __global__ void __launch_bounds__(TcdCfg<MT>::Threads, 1) tcd_kernel(const __gri
       }
     }
   } else if (warp == 3) {
+    if (TCD_TRACE_ON && (p.dbg & 1024)) {
+      // timing experiment: no scale / zero stager (the stage barrier expects the weight TMA only)
+    } else {
     // ---- scale / zero stager: tile t's row slices s[g, nt*128 : +128] and z[g, ...] (256 B each)
     // go into the side area of its stage (after the R weight tiles).  Lane l copies columns
     // 4l .. 4l+3 with 8-byte cp.async (global -> shared, no registers), and after the stage's
@@ -464,6 +468,7 @@ __global__ void __launch_bounds__(TcdCfg<MT>::Threads, 1) tcd_kernel(const __gri
           ph ^= 1;
         }
       }
+    }
     }
   } else {
     // ------------------------------ dequant groups ------------------------------
