@@ -81,7 +81,8 @@ class FusedGather:
     """Row f3: gathered outputs of an [M, N] column-sharded layer with the all-gather fused into the
     matmul epilogue.  Holds `nbuf` gathered buffers [M, N] and one flag array [world] per rank,
     mapped into every rank through CUDA IPC handles exchanged once over `group`.  Successive calls
-    alternate the buffers (the ordering contract of tl_matmul_gathered)."""
+    alternate the buffers (the ordering contract of tl_matmul_gathered): the Y a call returns stays
+    valid until the call `nbuf` calls later, whose peers write into the same buffer."""
 
     def __init__(self, M: int, N: int, world: int, rank: int, group=None, nbuf: int = 2,
                  dtype=torch.float16):
