@@ -432,29 +432,37 @@ __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_consta
           // distributed: contributor ci of S reduces elements [ci*nvt/S, (ci+1)*nvt/S) of each tile
           const int S = hi - lo + 1, ci = p.dist ? cta - lo : 0, SS = p.dist ? S : 1;
           const int ebeg = (int)((int64_t)ci * nvt / SS), nv = (int)((int64_t)(ci + 1) * nvt / SS);
+          // loads in flight per thread per round: kC contributors x kJ float4 (TC2_RED_J / TC2_RED_C)
+#ifndef TC2_RED_J
+#define TC2_RED_J 4
+#endif
+#ifndef TC2_RED_C
+#define TC2_RED_C 4
+#endif
+          constexpr int kJ = TC2_RED_J, kC = TC2_RED_C;
           for (int tj = 0; tj < (two ? 2 : 1); ++tj) {
             const float* pb = p.partial + (int64_t)tj * NB * kBN;
-            for (int e0 = ebeg + tid; e0 < nv; e0 += 4 * kTc2Groups * 128) {
-              float4 acc[4];
+            for (int e0 = ebeg + tid; e0 < nv; e0 += kJ * kTc2Groups * 128) {
+              float4 acc[kJ];
 #pragma unroll
-              for (int j = 0; j < 4; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-              for (int qb = lo; qb <= hi; qb += 4) {
-                float4 v[4][4];
+              for (int j = 0; j < kJ; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+              for (int qb = lo; qb <= hi; qb += kC) {
+                float4 v[kC][kJ];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
+                for (int c = 0; c < kC; ++c) {
                   const int qc = qb + c;
                   const float4* src =
                       reinterpret_cast<const float4*>(pb + (int64_t)(qc * 2 + (qc == lo ? flag[3] : 0)) * sstride);
 #pragma unroll
-                  for (int j = 0; j < 4; ++j) {
+                  for (int j = 0; j < kJ; ++j) {
                     const int e = e0 + j * kTc2Groups * 128;
                     v[c][j] = (qc <= hi && e < nv) ? __ldcg(src + e) : make_float4(0.f, 0.f, 0.f, 0.f);
                   }
                 }
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
+                for (int c = 0; c < kC; ++c)
 #pragma unroll
-                  for (int j = 0; j < 4; ++j)
+                  for (int j = 0; j < kJ; ++j)
                     if (qb + c <= hi) {
                       acc[j].x += v[c][j].x;
                       acc[j].y += v[c][j].y;
@@ -463,7 +471,7 @@ __global__ void __launch_bounds__(kTc2Threads, 1) tc2_kernel(const __grid_consta
                     }
               }
 #pragma unroll
-              for (int j = 0; j < 4; ++j) {
+              for (int j = 0; j < kJ; ++j) {
                 const int e = e0 + j * kTc2Groups * 128;
                 if (e < nv) {
                   const int m = e >> 5, c4 = e & 31;  // kBN / 4 == 32 float4 per row
