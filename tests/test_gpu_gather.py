@@ -154,3 +154,44 @@ def test_row_parallel_reduce_scatter_virtual_ranks(env, world, M, fmt, K, N, G):
     wd = dequant(parse_wtype(fmt), codes, s, z, G)
     rr = tolerance_check(Yg, matmul_fp64(A, wd), A, wd)
     assert rr["ok"], rr
+
+
+@pytest.mark.parametrize("act,M", [("bf16", 1), ("bf16", 64), ("i8", 1), ("i8", 40)])
+def test_gathered_other_activation_types(env, act, M):
+    """The fused gathered epilogue with bf16 activations / outputs and with int8 activations (staged
+    to fp16 before the fused kernel), two virtual ranks."""
+    import ml_dtypes
+    P, torch, dist = env
+    world, fmt, K, N, G = 2, "u4", 1024, 512, 128
+    w = P.wtype(fmt)
+    seed = wl.stable_seed("gather-act", act, M)
+    codes = wl.gen_codes(fmt, K, N, seed)
+    s = wl.gen_scales(fmt, K, N, G, seed)
+    z = wl.gen_zeros(fmt, K, N, G, seed, zero_range="full")
+    if act == "bf16":
+        BF = ml_dtypes.bfloat16
+        A = wl.gen_activations(M, K, seed).astype(np.float32).astype(BF)
+        s, z = s.astype(np.float32).astype(BF), z.astype(np.float32).astype(BF)
+        dev_t = lambda x: torch.from_numpy(np.ascontiguousarray(x).view(np.int16)).cuda().view(torch.bfloat16)
+        ydt, atype, out_kind = torch.bfloat16, P.TL_ACT_BF16, "bf16"
+    else:
+        A = wl.gen_activations_i8(M, K, seed)
+        dev_t = lambda x: to_dev(x, torch)
+        ydt, atype, out_kind = torch.float16, P.TL_ACT_I8, "f16"
+    Yg = [torch.full((M, N), float("nan"), dtype=ydt, device="cuda") for _ in range(world)]
+    flags = [torch.zeros(world, dtype=torch.int32, device="cuda") for _ in range(world)]
+    for r in range(world):
+        n0, n1 = dist.column_shard(N, world, r)
+        _, _, wt = prepare_weights(P, torch, fmt, K, n1 - n0, np.ascontiguousarray(codes[:, n0:n1]))
+        ys, fs = dist.peer_pointers([t.data_ptr() for t in Yg], [t.data_ptr() for t in flags], r, n0)
+        P.tl_matmul_gathered(w, M, n1 - n0, K, G, dev_t(A), wt, dev_t(s[:, n0:n1]), dev_t(z[:, n0:n1]), Yg[r][:, n0:],
+                             N, ys, fs, P.alloc_workspace(w, M, n1 - n0, K, G, atype=atype))
+    for r in range(world):
+        P.tl_gather_wait(flags[r], world, r, 1)
+    torch.cuda.synchronize()
+    outs = [(Yg[r].view(torch.int16).cpu().numpy().view(ml_dtypes.bfloat16) if act == "bf16" else Yg[r].cpu().numpy())
+            for r in range(world)]
+    assert np.array_equal(outs[0].view(np.uint16), outs[1].view(np.uint16))
+    wd = dequant(parse_wtype(fmt), codes, s, z, G)
+    rr = tolerance_check(outs[0], matmul_fp64(A, wd), A, wd, out_kind)
+    assert rr["ok"], rr
