@@ -424,7 +424,8 @@ def run_ours(args):
 def run_spectrum(args, P, torch, dev, peaks):
     """North-star coverage (every bit width 1-8, int / uint / float, PAPER.md:518-523 fig:exp_coverage):
     all 37 kernel formats on the four Llama-3.3-70B layers at M = 1 and M = 16 (gate_up at M = 16
-    is the paper's coverage shape BS=16, K=8192, N=57344).  Device time of one tl_matmul_ex per
+    is the paper's coverage shape BS=16, K=8192, N=57344), and gate_up at M = 128 (the batch-128
+    target, with the fraction of the dense fp16 peak).  Device time of one tl_matmul_ex per
     (format, layer, M), 10 back-to-back launches after 3 warm-ups; algorithmic GB/s and the fraction
     of the measured HBM copy bandwidth."""
     from oracle import all_kernel_formats
@@ -441,8 +442,9 @@ def run_spectrum(args, P, torch, dev, peaks):
             del codes
             s = wl.gen_scales_torch(fmt, K, N, G, seed, dev)
             z = wl.gen_zeros_torch(fmt, K, N, G, seed, dev)
-            ws = torch.zeros(P.tl_matmul_workspace_bytes(w, 16, N, K, G), dtype=torch.uint8, device=dev)
-            for M in (1, 16):
+            ws = torch.zeros(max(P.tl_matmul_workspace_bytes(w, 16, N, K, G),
+                                 P.tl_matmul_workspace_bytes(w, 128, N, K, G)), dtype=torch.uint8, device=dev)
+            for M in ((1, 16, 128) if lname == "gate_up" else (1, 16)):
                 A = wl.gen_activations_torch(M, K, seed, dev)
                 Y = torch.empty((M, N), dtype=torch.float16, device=dev)
                 for _ in range(3):
@@ -454,9 +456,14 @@ def run_spectrum(args, P, torch, dev, peaks):
                 torch.cuda.synchronize()
                 us = e0.elapsed_time(e1) / 10 * 1e3
                 b = alg_bytes(fmt, M, K, N, G)
-                out.append({"fmt": fmt, "layer": lname, "M": M, "us": round(us, 2),
-                            "GBps": round(b / (us * 1e-6) / 1e9, 1),
-                            "hbm_frac": round(b / (us * 1e-6) / 1e9 / peaks["hbm_gbs"], 3)})
+                rec = {"fmt": fmt, "layer": lname, "M": M, "us": round(us, 2),
+                       "GBps": round(b / (us * 1e-6) / 1e9, 1),
+                       "hbm_frac": round(b / (us * 1e-6) / 1e9 / peaks["hbm_gbs"], 3)}
+                if M == 128:  # tensor-bound for b <= 7: the fraction of the dense fp16 peak
+                    fl = 2 * M * K * N
+                    rec["TFLOPs"] = round(fl / (us * 1e-6) / 1e12, 1)
+                    rec["tensor_frac_fp16"] = round(fl / (us * 1e-6) / 1e12 / peaks["bf16_tflops"], 3)
+                out.append(rec)
             del wt, s, z, ws
     return out
 
