@@ -163,7 +163,9 @@ def cpu_baseline(formats, layers, G, M, budget_s=12.0, impl_line=False):
     global _CPU_POOL
     try:
         if _CPU_POOL is None:  # one pool per process, reused by every call (the reference arm's steps)
+            import atexit
             _CPU_POOL = cf.ProcessPoolExecutor(max_workers=cores, mp_context=mp.get_context("spawn"))
+            atexit.register(_CPU_POOL.shutdown, wait=True)
             list(_CPU_POOL.map(_cpu_task, tasks[:cores], chunksize=1))  # start-up of the workers, untimed
         ex = _CPU_POOL
         w0 = time.perf_counter()
