@@ -272,6 +272,13 @@ tl_status tl_reduce_scatter_peer(tl_atype a, const void* const* parts, int32_t n
 tl_status tl_mx_scales_to_f16(const uint8_t* e8m0, int64_t count, int32_t exp_adjust, void* scales_f16,
                               void* stream);
 
+/* The same conversion into bf16 scales, for bf16 activations (scales have the activation type): bf16
+ * carries E8M0's 8 exponent bits, so with exp_adjust = 0 every code except the NaN code 0xFF is
+ * exact (e = 0 is the bf16 subnormal 2^-127); values outside 2^-133 .. 2^127 and 0xFF become NaN.
+ * Errors as tl_mx_scales_to_f16. */
+tl_status tl_mx_scales_to_bf16(const uint8_t* e8m0, int64_t count, int32_t exp_adjust, void* scales_bf16,
+                               void* stream);
+
 /* Test hook: out[K,N] fp32 = (value(q) - z) * s, computed exactly in fp32 from
  * the TRANSFORMED weight (reading R9: exact, so it is bit-comparable with the
  * oracle's dequant). */

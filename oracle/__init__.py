@@ -34,10 +34,10 @@ from .packing import pack, unpack, packed_nbytes
 from .dequant import dequant
 from .matmul import matmul_fp64, matmul_cols_fp64, tolerance_check
 from .quantize import encode
-from .mx import e8m0_value, e8m0_to_f16_scale, mx_dequant, MX_BLOCK
+from .mx import e8m0_value, e8m0_to_f16_scale, e8m0_to_bf16_scale, mx_dequant, MX_BLOCK
 
 __all__ = [
     "WType", "parse_wtype", "all_kernel_formats", "oracle_only_formats", "code_values",
     "pack", "unpack", "packed_nbytes", "dequant", "matmul_fp64", "matmul_cols_fp64",
-    "tolerance_check", "encode", "e8m0_value", "e8m0_to_f16_scale", "mx_dequant", "MX_BLOCK",
+    "tolerance_check", "encode", "e8m0_value", "e8m0_to_f16_scale", "e8m0_to_bf16_scale", "mx_dequant", "MX_BLOCK",
 ]

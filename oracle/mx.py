@@ -37,6 +37,15 @@ def e8m0_to_f16_scale(e: np.ndarray, exp_adjust: int = 0) -> np.ndarray:
     return np.where(ok, v, np.nan).astype(np.float16)
 
 
+def e8m0_to_bf16_scale(e: np.ndarray, exp_adjust: int = 0) -> np.ndarray:
+    """The library's bf16 group scale for an E8M0 code (bf16 activations): the exact value when it is
+    a bf16 number (2^-133 .. 2^127), else NaN (R25).  Returned as float64 values."""
+    v = e8m0_value(e, exp_adjust)
+    x = np.asarray(e).astype(np.int64) - 127 + exp_adjust
+    ok = np.isfinite(v) & (x >= -133) & (x <= 127)
+    return np.where(ok, v, np.nan)
+
+
 def mx_dequant(wt: WType, codes: np.ndarray, e8m0: np.ndarray, exp_adjust: int = 0) -> np.ndarray:
     """codes [K,N] uint8, e8m0 [K/32,N] uint8 -> w [K,N] float64 = value(code) * 2^(e-127+adj).
 

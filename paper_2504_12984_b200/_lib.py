@@ -108,13 +108,14 @@ _tl_reduce_scatter_peer = _sig("tl_reduce_scatter_peer", ctypes.c_int,
                                [ctypes.c_int, ctypes.POINTER(_vp), _i32, _i64, _i64, _i64, _vp, _i64, _vp])
 _tl_gather_wait = _sig("tl_gather_wait", ctypes.c_int, [_vp, _i32, _i32, _u32, _vp])
 _tl_mx_scales_to_f16 = _sig("tl_mx_scales_to_f16", ctypes.c_int, [_vp, _i64, _i32, _vp, _vp])
+_tl_mx_scales_to_bf16 = _sig("tl_mx_scales_to_bf16", ctypes.c_int, [_vp, _i64, _i32, _vp, _vp])
 _tl_dequant = _sig("tl_dequant", ctypes.c_int, [_W, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _vp])
 _tl_status_str = _sig("tl_status_str", ctypes.c_char_p, [ctypes.c_int])
 _tl_last_error = _sig("tl_last_error", ctypes.c_char_p, [])
 
 EXPORTED = ["tl_packed_bytes", "tl_transformed_bytes", "tl_format_version", "tl_pack", "tl_unpack",
             "tl_transform_weights", "tl_untransform_weights", "tl_matmul_workspace_bytes", "tl_matmul",
-            "tl_matmul_ex", "tl_matmul_hostio", "tl_matmul_batch_hostio", "tl_matmul_plan", "tl_matmul_gathered", "tl_gather_wait", "tl_signal_peers", "tl_reduce_scatter_peer", "tl_mx_scales_to_f16", "tl_dequant", "tl_status_str",
+            "tl_matmul_ex", "tl_matmul_hostio", "tl_matmul_batch_hostio", "tl_matmul_plan", "tl_matmul_gathered", "tl_gather_wait", "tl_signal_peers", "tl_reduce_scatter_peer", "tl_mx_scales_to_f16", "tl_mx_scales_to_bf16", "tl_dequant", "tl_status_str",
             "tl_last_error"]
 
 
@@ -249,6 +250,17 @@ def tl_reduce_scatter_peer(parts: list[int], M: int, N: int, ldp: int, Y: torch.
     _check(_tl_reduce_scatter_peer(atype, pa, n, M, N, ldp, Y.data_ptr(), ldy if ldy is not None else N,
                                    _stream(stream)), "tl_reduce_scatter_peer")
     return Y
+
+
+def tl_mx_scales_to_bf16(e8m0: torch.Tensor, exp_adjust: int = 0, out: torch.Tensor | None = None,
+                         stream=None) -> torch.Tensor:
+    """E8M0 block-scale codes (uint8) -> bf16 scales 2^(e-127+exp_adjust) (exact for every finite code)."""
+    if e8m0.dtype != torch.uint8:
+        raise ValueError("e8m0 must be uint8")
+    out = out if out is not None else torch.empty(e8m0.shape, dtype=torch.bfloat16, device=e8m0.device)
+    _check(_tl_mx_scales_to_bf16(_ptr(e8m0), e8m0.numel(), exp_adjust, _ptr(out), _stream(stream)),
+           "tl_mx_scales_to_bf16")
+    return out
 
 
 def tl_mx_scales_to_f16(e8m0: torch.Tensor, exp_adjust: int = 0, out: torch.Tensor | None = None,

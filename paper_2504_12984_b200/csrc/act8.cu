@@ -85,9 +85,38 @@ __global__ void mx_scales_kernel(const uint8_t* __restrict__ e8m0, int64_t count
   }
 }
 
+// E8M0 code e -> bf16 2^(e - 127 + adj): bf16 has E8M0's 8 exponent bits, so every finite code is
+// exact when adj = 0 (e = 0 gives the bf16 subnormal 2^-127); out of range (|x| beyond
+// 2^-133 .. 2^127) or the NaN code 0xFF -> NaN.
+__global__ void mx_scales_bf16_kernel(const uint8_t* __restrict__ e8m0, int64_t count, int adj,
+                                      unsigned short* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    const int e = e8m0[i];
+    const int x = e - 127 + adj;  // the scale is 2^x
+    unsigned short h;
+    if (e == 0xFF || x > 127 || x < -133) h = 0x7FC0u;                 // NaN
+    else if (x >= -126) h = (unsigned short)((x + 127) << 7);            // normal: biased exponent x + 127
+    else h = (unsigned short)(1u << (x + 133));                          // subnormal: 2^x = m * 2^-133
+    out[i] = h;
+  }
+}
+
 }  // namespace tl
 
 using namespace tl;
+
+extern "C" tl_status tl_mx_scales_to_bf16(const uint8_t* e8m0, int64_t count, int32_t exp_adjust, void* scales_bf16,
+                                          void* stream) {
+  if (count < 0) return fail(TL_EINVAL_SHAPE, "count=%lld < 0", (long long)count);
+  if (count == 0) return TL_OK;
+  if (!e8m0 || !scales_bf16) return fail(TL_ENULL, "tl_mx_scales_to_bf16: NULL pointer");
+  if (exp_adjust < -64 || exp_adjust > 64) return fail(TL_EINVAL_SHAPE, "exp_adjust=%d outside [-64, 64]", exp_adjust);
+  int blocks = (int)((count + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  mx_scales_bf16_kernel<<<blocks, 256, 0, as_stream(stream)>>>(e8m0, count, exp_adjust,
+                                                               reinterpret_cast<unsigned short*>(scales_bf16));
+  return check_launch("mx_scales_bf16_kernel");
+}
 
 extern "C" tl_status tl_mx_scales_to_f16(const uint8_t* e8m0, int64_t count, int32_t exp_adjust, void* scales_f16,
                                          void* stream) {

@@ -141,3 +141,41 @@ def test_mx_matmul(env, fmt, adj, center, M):
     r = tolerance_check(Y.cpu().numpy(), matmul_fp64(A, wd), A, wd)
     assert r["ok"], r
     assert r["max_abs_ratio"] <= GUARD, r
+
+
+@pytest.mark.parametrize("adj", [0, -6, -10])
+def test_mx_scales_bf16_all_codes(env, adj):
+    import ml_dtypes
+    from oracle import e8m0_to_bf16_scale
+    P, torch = env
+    e = torch.arange(256, dtype=torch.int32).to(torch.uint8).cuda()
+    got = P.tl_mx_scales_to_bf16(e, adj).view(torch.int16).cpu().numpy().view(ml_dtypes.bfloat16).astype(np.float64)
+    want = e8m0_to_bf16_scale(np.arange(256, dtype=np.uint8), adj)
+    assert np.array_equal(np.isnan(got), np.isnan(want))
+    ok = ~np.isnan(want)
+    assert np.array_equal(got[ok], want[ok])
+
+
+@pytest.mark.parametrize("M", [1, 24])
+@pytest.mark.parametrize("fmt,adj,center", [("f4e2m1", 0, 119), ("f8e4m3", 0, 115), ("i8", -6, 121)])
+def test_mx_matmul_bf16(env, fmt, adj, center, M):
+    """MX weights with bf16 activations: bf16 block scales from tl_mx_scales_to_bf16, group 32."""
+    import ml_dtypes
+    P, torch = env
+    BF = ml_dtypes.bfloat16
+    K, N = 1024, 256
+    seed = wl.stable_seed("mx-bf16", fmt, M)
+    A = wl.gen_activations(M, K, seed).astype(np.float32).astype(BF)
+    codes = wl.gen_codes(fmt, K, N, seed)
+    e = wl.gen_mx_exponents(K, N, seed, center)
+    w, _, wt = prepare_weights(P, torch, fmt, K, N, codes)
+    s_d = P.tl_mx_scales_to_bf16(to_dev(e, torch), adj)
+    A_d = torch.from_numpy(np.ascontiguousarray(A).view(np.int16)).cuda().view(torch.bfloat16)
+    Y = torch.full((M, N), float("nan"), dtype=torch.bfloat16, device="cuda")
+    ws = P.alloc_workspace(w, M, N, K, 32, atype=P.TL_ACT_BF16)
+    P.tl_matmul(w, M, N, K, 32, A_d, wt, s_d, None, Y, ws)
+    torch.cuda.synchronize()
+    Yn = Y.view(torch.int16).cpu().numpy().view(BF)
+    wd = mx_dequant(parse_wtype(fmt), codes, e, adj)
+    r = tolerance_check(Yn, matmul_fp64(A, wd), A, wd, "bf16")
+    assert r["ok"], r

@@ -69,3 +69,23 @@ def test_mx_dequant_matches_ocp_element_and_scale_types(fmt, mlt, adj):
 def test_mx_dequant_rejects_bad_block_shape():
     with pytest.raises(ValueError):
         mx_dequant(parse_wtype("f4e2m1"), np.zeros((64, 8), np.uint8), np.zeros((1, 8), np.uint8))
+
+
+@pytest.mark.parametrize("adj", [0, -6, -10, 3])
+def test_bf16_scale_is_exact_in_range(adj):
+    from oracle import e8m0_to_bf16_scale
+    v = e8m0_to_bf16_scale(ALL, adj)
+    x = ALL.astype(np.int64) - 127 + adj
+    for e in range(256):
+        xe = int(x[e])
+        if e == 255 or xe < -133 or xe > 127:
+            assert np.isnan(v[e]), e
+        else:
+            b = np.array([v[e]]).astype(ml_dtypes.bfloat16)
+            assert float(b[0]) == 2.0 ** xe  # representable in bf16, hence exact
+            bits = int(b.view(np.uint16)[0])
+            # IEEE-style bf16: normal 2^x has biased exponent x+127, subnormal (x < -126) bit x+133
+            assert bits == (((xe + 127) << 7) if xe >= -126 else (1 << (xe + 133))), (e, hex(bits))
+    # with adj = 0 every finite E8M0 code is a bf16 number (the reason bf16 scales need no range check)
+    if adj == 0:
+        assert not np.isnan(v[:255]).any()
