@@ -426,6 +426,9 @@ def run_ours(args):
     # ---- north-star coverage: all 37 formats x 70B layers x M in {1, 16} (rank 0 only) ----
     spectrum = run_spectrum(args, P, torch, dev, peaks) if (rank == 0 and not args.no_spectrum) else None
 
+    # ---- BASELINE configs[1] (C2): Llama-3-8B decode layers x 22 formats x M in {1, 16} (rank 0) ----
+    c2 = run_c2(args, P, torch, dev, peaks) if (rank == 0 and not args.no_spectrum) else None
+
     # ---- row f4: int8 activations and MX weights (rank 0 only) ----
     f4 = run_f4(args, P, torch, dev, peaks) if (rank == 0 and not args.no_spectrum) else None
 
@@ -453,6 +456,7 @@ def run_ours(args):
             "details_c5": c5,
             "details_spectrum": spectrum,
             "details_f4": f4,
+            "details_c2": c2,
         }
         if world == 1 and not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline(args.formats, layers, G, M)
@@ -504,6 +508,42 @@ def run_spectrum(args, P, torch, dev, peaks):
                     rec["TFLOPs"] = round(fl / (us * 1e-6) / 1e12, 1)
                     rec["tensor_frac_fp16"] = round(fl / (us * 1e-6) / 1e12 / peaks["bf16_tflops"], 3)
                 out.append(rec)
+            del wt, s, z, ws
+    return out
+
+
+def run_c2(args, P, torch, dev, peaks):
+    """BASELINE configs[1] / SURVEY C2: the Llama-3-8B decode linear layers (q, k, v, o, gate_up, down)
+    at M = 1 and 16 for the 22 formats of P:521's coverage (uint1..8, int1..8, f3e1m1, f4e2m1,
+    f5e2m2, f6e3m2, f7e3m3, f8e4m3), group 128: device time of one tl_matmul_ex (10 back-to-back
+    launches after 3 warm-ups), algorithmic GB/s and the fraction of the measured HBM bandwidth.
+    The 8B layers are 0.5-121 MB: the smaller ones sit below the per-launch floor."""
+    G = 128
+    out = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for fmt in wl.CONFIG1_FORMATS:
+        w = P.wtype(fmt)
+        for lname, (K, N) in wl.LLAMA3_8B.items():
+            seed = wl.stable_seed("c2", fmt, lname)
+            wt = P.tl_transform_weights(w, K, N, P.tl_pack(w, K, N, wl.gen_codes_torch(fmt, K, N, seed, dev)))
+            s = wl.gen_scales_torch(fmt, K, N, G, seed, dev)
+            z = wl.gen_zeros_torch(fmt, K, N, G, seed, dev)
+            ws = torch.zeros(P.tl_matmul_workspace_bytes(w, 16, N, K, G), dtype=torch.uint8, device=dev)
+            for M in (1, 16):
+                A = wl.gen_activations_torch(M, K, seed, dev)
+                Y = torch.empty((M, N), dtype=torch.float16, device=dev)
+                for _ in range(3):
+                    P.tl_matmul_ex(w, M, N, K, G, A, wt, s, z, Y, ws, flags=P.TL_FLAG_STATIC_WEIGHTS)
+                e0.record()
+                for _ in range(10):
+                    P.tl_matmul_ex(w, M, N, K, G, A, wt, s, z, Y, ws, flags=P.TL_FLAG_STATIC_WEIGHTS)
+                e1.record()
+                torch.cuda.synchronize()
+                us = e0.elapsed_time(e1) / 10 * 1e3
+                b = alg_bytes(fmt, M, K, N, G)
+                out.append({"fmt": fmt, "layer": lname, "M": M, "us": round(us, 2),
+                            "GBps": round(b / (us * 1e-6) / 1e9, 1),
+                            "hbm_frac": round(b / (us * 1e-6) / 1e9 / peaks["hbm_gbs"], 3)})
             del wt, s, z, ws
     return out
 
