@@ -639,8 +639,23 @@ def run_c5(args, P, torch, dist, world, rank, dev, peaks):
             A = wl.gen_activations_torch(M, K, wl.stable_seed("c5A", M), dev)
             Y = torch.empty((M, Ns), dtype=torch.float16, device=dev)
             res = {}
-            for variant in ("sharded", "gathered"):
+            fg = None
+            variants = ["sharded", "gathered"]
+            if args.fused_gather:
+                # row f3: the all-gather fused into the epilogue over NVLink peer memory (opt-in)
+                from paper_2504_12984_b200.dist import FusedGather, peer_pointers
+                fg = FusedGather(M, N, world, rank)
+                variants.append("fused")
+            for variant in variants:
                 def once():
+                    if variant == "fused":
+                        fg.epoch += 1
+                        b = fg.epoch % fg.nbuf
+                        ys, fs = peer_pointers(fg.y_bases[b], fg.f_bases, rank, n0)
+                        P.tl_matmul_gathered(w, M, Ns, K, G, A, wt, s, z, fg.Yg[b][:, n0:], N, ys, fs, ws,
+                                             flags=P.TL_FLAG_STATIC_WEIGHTS)
+                        P.tl_gather_wait(fg.flags, world, rank, fg.epoch)
+                        return
                     P.tl_matmul_ex(w, M, Ns, K, G, A, wt, s, z, Y, ws, flags=P.TL_FLAG_STATIC_WEIGHTS)
                     if variant == "gathered" and world > 1:
                         gather_columns(Y, N, world)
@@ -664,6 +679,7 @@ def run_c5(args, P, torch, dist, world, rank, dev, peaks):
             byts = alg_bytes(fmt, M, K, N, G)
             out.append({"fmt": fmt, "M": M, "P": world, "shard_cols": Ns, "sharded_us": round(res["sharded"], 2),
                         "gathered_us": round(res["gathered"], 2),
+                        "fused_gathered_us": round(res["fused"], 2) if "fused" in res else None,
                         "GBps_total": round(byts / (res["sharded"] * 1e-6) / 1e9, 1),
                         "hbm_frac_per_gpu": round(byts / world / (res["sharded"] * 1e-6) / 1e9 / peaks["hbm_gbs"], 3),
                         "TFLOPs_total": round(2 * M * K * N / (res["sharded"] * 1e-6) / 1e12, 2)})
@@ -703,6 +719,8 @@ def main():
     ap.add_argument("--formats", nargs="+", default=wl.CONFIG2["formats"])
     ap.add_argument("--layers", nargs="+", default=list(wl.LLAMA33_70B))
     ap.add_argument("--gather", action="store_true")
+    ap.add_argument("--fused-gather", action="store_true",
+                    help="details_c5 also times the all-gather fused into the epilogue (row f3, CUDA IPC peers)")
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -72,6 +72,8 @@ def peer_pointers(y_bases: list[int], flag_bases: list[int], rank: int, n0: int,
 
 def exchange(obj, world: int, group=None) -> list:
     """All ranks' `obj` (picklable), rank order (one torch.distributed all_gather_object)."""
+    if world == 1:
+        return [obj]
     out = [None] * world
     dist.all_gather_object(out, obj, group=group)
     return out
