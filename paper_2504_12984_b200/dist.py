@@ -93,7 +93,7 @@ class FusedGather:
         self.Yg = [torch.empty((M, N), dtype=dtype, device="cuda") for _ in range(nbuf)]
         self.flags = torch.zeros(world, dtype=torch.int32, device="cuda")
         torch.cuda.synchronize()
-        mine = [reduce_tensor(t) for t in self.Yg + [self.flags]]
+        mine = [reduce_tensor(t) for t in self.Yg + [self.flags]] if world > 1 else None
         self._peer_tensors = []     # keeps the IPC mappings alive
         y_bases = [[0] * world for _ in range(nbuf)]
         f_bases = [0] * world
@@ -146,7 +146,7 @@ class FusedReduceScatter:
         self.parts = [torch.empty((M, N), dtype=dtype, device="cuda") for _ in range(nbuf)]
         self.flags = torch.zeros(world, dtype=torch.int32, device="cuda")
         torch.cuda.synchronize()
-        mine = [reduce_tensor(t) for t in self.parts + [self.flags]]
+        mine = [reduce_tensor(t) for t in self.parts + [self.flags]] if world > 1 else None
         self._peer_tensors = []
         self.p_bases = [[0] * world for _ in range(nbuf)]
         self.f_bases = [0] * world
