@@ -250,3 +250,31 @@ def test_prefill_chunks_and_auto_dispatch(env):
     w = dequant(parse_wtype(fmt), codes[:, cols], s[:, cols], z[:, cols], G)
     r = tolerance_check(Y[:, cols], Y64, A, w)
     assert r["ok"] and r["max_abs_ratio"] <= 1e-3, r
+
+
+@pytest.mark.parametrize("fmt,M,K,N", [("u3", 128, 2048, 1280), ("i5", 64, 4096, 1024), ("f6e3m2", 100, 1024, 2560),
+                                       ("u8", 128, 8192, 512)])
+def test_distributed_reduction_same_bits_as_last_arriver(env, fmt, M, K, N):
+    """The batched kernel's distributed stream-K reduction (aligned split grids, every contributor
+    reduces 1/S of the tile) sums the contributors in the same CTA order as the last-arriver
+    reduction (TL_TC2_DIST=0): the outputs must be bit-identical, and identical run to run."""
+    import os
+    P, torch = env
+    G = 128
+    A, codes, s, z = make_problem(fmt, M, K, N, G, seed_tag="dist")
+    w, _, wt = prepare_weights(P, torch, fmt, K, N, codes)
+    outs = []
+    for dist in ("1", "0", "1"):
+        old = os.environ.get("TL_TC2_DIST")
+        os.environ["TL_TC2_DIST"] = dist
+        try:
+            Y, _, ws = run_matmul(P, torch, fmt, A, codes, s, z, G, path=2, wt=wt)
+        finally:
+            if old is None:
+                os.environ.pop("TL_TC2_DIST", None)
+            else:
+                os.environ["TL_TC2_DIST"] = old
+        assert int(ws[: 64 * 1024].view(torch.int32).abs().sum().item()) == 0  # semaphores back at zero
+        outs.append(Y.view(np.uint16).copy())
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    check_oracle(fmt, A, codes, s, z, G, outs[0].view(np.float16))
