@@ -195,3 +195,26 @@ def test_gathered_other_activation_types(env, act, M):
     wd = dequant(parse_wtype(fmt), codes, s, z, G)
     rr = tolerance_check(outs[0], matmul_fp64(A, wd), A, wd, out_kind)
     assert rr["ok"], rr
+
+
+def test_fused_classes_single_rank(env):
+    """dist.FusedGather / dist.FusedReduceScatter at world size 1 (no peers, no IPC): the plumbing of
+    epochs, buffers and waits around tl_matmul_gathered / tl_signal_peers / tl_reduce_scatter_peer."""
+    P, torch, dist = env
+    fmt, M, K, N, G = "u4", 2, 1024, 512, 128
+    A, codes, s, z = _problem(fmt, M, K, N, G, "fused-classes")
+    wd = dequant(parse_wtype(fmt), codes, s, z, G)
+    Y64 = matmul_fp64(A, wd)
+    layer = dist.ShardedA16WxLinear(fmt, K, N, G, to_dev(codes, torch), to_dev(s, torch), to_dev(z, torch), 1, 0)
+    fg = dist.FusedGather(M, N, 1, 0)
+    for _ in range(3):  # three epochs over two alternating buffers
+        Y = fg(layer, to_dev(A, torch))
+        torch.cuda.synchronize()
+        assert tolerance_check(Y.cpu().numpy(), Y64, A, wd)["ok"]
+    rs = dist.FusedReduceScatter(M, N, 1, 0)
+    w, _, wt = prepare_weights(P, torch, fmt, K, N, codes)
+    ws = P.alloc_workspace(w, M, N, K, G)
+    for _ in range(3):
+        Y = rs(w, K, G, to_dev(A, torch), wt, to_dev(s, torch), to_dev(z, torch), ws)
+        torch.cuda.synchronize()
+        assert tolerance_check(Y.cpu().numpy(), Y64, A, wd)["ok"]
