@@ -367,9 +367,19 @@ def run_ours(args):
 
     # ---- extra batch sizes (reported, not part of `value`) ----
     extra = []
+    extra_steps = []
     if not args.no_extra:
         for m2 in [x for x in (16, 64, 128) if x != M]:
-            ms2, lms2 = timed(m2, max(3, min(args.steps, 10)), 2, per_launch=True)
+            n2 = max(3, min(args.steps, 10))
+            ms2, lms2 = timed(m2, n2, 2, per_launch=True)
+            # the whole 16-launch step at this batch (one graph, launches overlapped): the throughput a
+            # caller sees; the per-launch rows below come from the serialising event graph
+            sb = sum(alg_bytes(p["fmt"], m2, p["K"], p["N"], G) for p in probs)
+            sf = sum(2 * m2 * p["K"] * p["N"] for p in probs)
+            st = ms2 / n2 * 1e-3
+            extra_steps.append({"M": m2, "step_us": round(st * 1e6, 1), "GBps": round(sb / st / 1e9, 1),
+                                "TFLOPs": round(sf / st / 1e12, 1),
+                                "tensor_frac_fp16": round(sf / st / 1e12 / peaks["bf16_tflops"], 3)})
             for i, p in enumerate(probs):
                 lm = statistics.mean(row[i] for row in lms2)
                 b = alg_bytes(p["fmt"], m2, p["K"], p["N"], G)
@@ -453,6 +463,7 @@ def run_ours(args):
             "clocks": sampler.summary(),
             "details": details,
             "details_extra_M": extra,
+            "details_extra_M_steps": extra_steps,
             "details_c5": c5,
             "details_spectrum": spectrum,
             "details_f4": f4,
